@@ -1,0 +1,204 @@
+"""Generate tests/golden/*.npz by running the UNMODIFIED reference.
+
+Run in the authoring container only (needs /root/reference):
+    python oracle/make_golden.py
+The fixtures are committed; nothing at test time on the GPU box reads
+/root/reference.  Inputs are seeded (numpy default_rng), so the script is
+reproducible.
+"""
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+from mfcg.dofs import (batch_size, compute_range_schedule, distribute_dofs,  # noqa: E402
+                       make_batches, renumber_optimized)
+from mfcg.mesh import GeometryVariant, build_cartesian_mesh, deform_mesh, precompute_geometry  # noqa: E402
+from mfcg.operator import MatrixFreeOperator, OperatorSpec  # noqa: E402
+from mfcg.solvers import SolverConfig, solve  # noqa: E402
+from mfcg.tensor import gauss_lobatto_quadrature, gauss_quadrature, lagrange_basis  # noqa: E402
+
+OUT = Path(__file__).resolve().parent.parent / "tests" / "golden"
+OUT.mkdir(parents=True, exist_ok=True)
+
+
+def build(cells, p, nq, *, constrain=True, numbering="default", traversal="morton", batch=None,
+          deform=0.0, variant=GeometryVariant.AFFINE, quadrature="gauss"):
+    mesh = build_cartesian_mesh(cells)
+    if deform:
+        mesh = deform_mesh(mesh, deform)
+    h = distribute_dofs(mesh, p, 1, constrain_boundary=constrain)
+    plan = make_batches(mesh, batch or batch_size(p, 1, 8), traversal)
+    if numbering == "optimized":
+        h = renumber_optimized(h, plan)
+    spec = OperatorSpec("laplace", 1, p, nq, variant, quadrature)
+    return MatrixFreeOperator(spec, mesh, h, plan), h, plan, mesh
+
+
+def hist_array(res):
+    return np.array([[e["alpha"], e["beta"], e["gamma"], e["residual"]] for e in res.history])
+
+
+def tables():
+    out = {}
+    for n in range(1, 11):
+        q = gauss_quadrature(n)
+        out[f"gauss_x_{n}"], out[f"gauss_w_{n}"] = q.points, q.weights
+        if n >= 2:
+            q = gauss_lobatto_quadrature(n)
+            out[f"gl_x_{n}"], out[f"gl_w_{n}"] = q.points, q.weights
+    for p in range(1, 9):
+        for nq in (p + 1, p + 2):
+            b = lagrange_basis(p, gauss_quadrature(nq))
+            out[f"S_{p}_{nq}"], out[f"D_{p}_{nq}"] = b.shape_values, b.shape_gradients
+        b = lagrange_basis(p, gauss_lobatto_quadrature(p + 1))
+        out[f"Dgl_{p}"] = b.shape_gradients
+    np.savez_compressed(OUT / "tables.npz", **out)
+
+
+NUMBERING_CASES = [
+    ((2, 2, 2), 1), ((2, 1, 1), 1), ((3, 4, 2), 2), ((2, 2, 2), 3), ((5, 3, 6), 5),
+    ((8, 8, 8), 4), ((4, 4, 4), 5), ((6, 6, 6), 1), ((7, 6, 5), 4),
+]
+
+
+def numbering():
+    out = {}
+    for cells, p in NUMBERING_CASES:
+        tag = "x".join(map(str, cells)) + f"_p{p}"
+        mesh = build_cartesian_mesh(cells)
+        h = distribute_dofs(mesh, p, 1, constrain_boundary=True)
+        out[f"{tag}_blocks"] = h.cell_index_blocks
+        out[f"{tag}_constrained"] = h.constrained_dofs
+        for trav in ("morton", "lexicographic"):
+            plan = make_batches(mesh, batch_size(p, 1, 8) if trav == "morton" else 3, trav)
+            out[f"{tag}_{trav}_order"] = np.concatenate(plan.batches)
+            out[f"{tag}_{trav}_bsize"] = np.array([plan.batch_size])
+            r = renumber_optimized(h, plan)
+            out[f"{tag}_{trav}_rblocks"] = r.cell_index_blocks
+            out[f"{tag}_{trav}_perm"] = r.permutation
+            out[f"{tag}_{trav}_rconstrained"] = r.constrained_dofs
+            s = compute_range_schedule(r, plan)
+            out[f"{tag}_{trav}_first"] = s.first_touch_batch
+            out[f"{tag}_{trav}_last"] = s.last_touch_batch
+    out["batch_sizes"] = np.array([batch_size(5, 3, 8), batch_size(5, 1, 8), batch_size(1, 1, 1),
+                                   batch_size(3, 1, 8), batch_size(9, 3, 1)])
+    np.savez_compressed(OUT / "numbering.npz", **out)
+
+
+# (cells, p, nq, numbering, constrain)
+APPLY_CASES = [
+    ((2, 2, 2), 3, 4, "default", True),
+    ((3, 4, 2), 2, 3, "default", True),
+    ((2, 3, 2), 1, 2, "default", True),
+    ((4, 4, 4), 5, 6, "optimized", True),
+    ((5, 4, 9), 5, 6, "default", True),
+    ((9, 5, 3), 5, 7, "optimized", True),
+    ((3, 3, 3), 7, 8, "default", True),
+    ((2, 3, 2), 8, 9, "default", True),
+    ((7, 6, 5), 4, 5, "optimized", True),
+    ((11, 7, 3), 3, 4, "default", True),
+    ((4, 3, 5), 6, 7, "default", True),
+    ((3, 3, 2), 4, 5, "default", False),
+    ((21, 12, 2), 2, 3, "default", True),
+    ((18, 17, 3), 1, 2, "optimized", True),
+]
+
+
+def apply_cases():
+    out = {}
+    for ci, (cells, p, nq, numb, con) in enumerate(APPLY_CASES):
+        op, h, plan, mesh = build(cells, p, nq, constrain=con, numbering=numb)
+        rng = np.random.default_rng(100 + ci)
+        u = rng.standard_normal(h.n_dofs)
+        out[f"c{ci}_u"] = u
+        out[f"c{ci}_Au"] = op.apply(u)
+        out[f"c{ci}_invdiag"] = op.compute_diagonal().inverse_diagonal
+        out[f"c{ci}_blocks"] = h.cell_index_blocks
+        out[f"c{ci}_constrained"] = h.constrained_dofs
+    np.savez_compressed(OUT / "apply.npz", **out)
+
+
+def config1():
+    """BASELINE.json configs[0]: 8^3 cells, Q4, 5-point Gauss, 100 fixed iterations."""
+    op, h, plan, mesh = build((8, 8, 8), 4, 5)
+    minv = op.compute_diagonal()
+    b = np.random.default_rng(0).uniform(-1.0, 1.0, h.n_dofs)
+    b[h.constrained_dofs] = 0.0
+    out = {"b": b, "invdiag": minv.inverse_diagonal, "Ab": op.apply(b)}
+    cfg = SolverConfig(fixed_iterations=100)
+    for variant in ("pcg", "combined_pcg", "cg", "combined_cg"):
+        res = solve(variant, op, b, minv=minv, config=cfg)
+        out[f"{variant}_hist"] = hist_array(res)
+        out[f"{variant}_x"] = res.x
+    # the reference's own re-ordering envelope: same maths, lexicographic batches
+    op2, h2, _, _ = build((8, 8, 8), 4, 5, traversal="lexicographic", batch=7)
+    for variant in ("pcg", "combined_pcg"):
+        res = solve(variant, op2, b, minv=op2.compute_diagonal(), config=cfg)
+        out[f"{variant}_hist_reordered"] = hist_array(res)
+        out[f"{variant}_x_reordered"] = res.x
+    # tolerance-terminated run (early exit semantics)
+    for variant in ("pcg", "combined_pcg"):
+        res = solve(variant, op, b, minv=minv, config=SolverConfig(tolerance=1e-6, max_iterations=500))
+        out[f"{variant}_tol_hist"] = hist_array(res)
+        out[f"{variant}_tol_iters"] = np.array([res.iterations, int(res.converged)])
+    np.savez_compressed(OUT / "config1.npz", **out)
+
+
+def q5_small():
+    """BASELINE.json configs[1], smallest rungs (4^3 and 6^3 cells, Q5), 200 iterations, plus
+    optimized numbering for 4^3."""
+    out = {}
+    for n, numb in ((4, "default"), (6, "default"), (4, "optimized")):
+        op, h, plan, mesh = build((n, n, n), 5, 6, numbering=numb)
+        minv = op.compute_diagonal()
+        b = np.random.default_rng(0).uniform(-1.0, 1.0, h.n_dofs)
+        if numb == "optimized":
+            bo = np.empty_like(b)
+            bo[h.permutation] = b
+            b = bo
+        b[h.constrained_dofs] = 0.0
+        tag = f"n{n}_{numb}"
+        out[f"{tag}_b"] = b
+        for variant in ("pcg", "combined_pcg"):
+            res = solve(variant, op, b, minv=minv, config=SolverConfig(fixed_iterations=200))
+            out[f"{tag}_{variant}_hist"] = hist_array(res)
+            out[f"{tag}_{variant}_x"] = res.x
+    np.savez_compressed(OUT / "q5_small.npz", **out)
+
+
+CURVED_CASES = [((3, 3, 3), 3, 4, 0.1), ((4, 3, 5), 5, 6, 0.1), ((2, 2, 2), 2, 4, 0.05)]
+
+
+def curved():
+    out = {}
+    for ci, (cells, p, nq, amp) in enumerate(CURVED_CASES):
+        op, h, plan, mesh = build(cells, p, nq, deform=amp, variant=GeometryVariant.FINAL_TENSOR_LOAD)
+        rng = np.random.default_rng(200 + ci)
+        u = rng.standard_normal(h.n_dofs)
+        out[f"k{ci}_u"] = u
+        out[f"k{ci}_Au"] = op.apply(u)
+        out[f"k{ci}_invdiag"] = op.compute_diagonal().inverse_diagonal
+        out[f"k{ci}_final_tensor"] = op.geometry.payload["final_tensor"]
+        g2 = precompute_geometry(mesh, GeometryVariant.INVERSE_JACOBIAN_LOAD, op.quadrature)
+        out[f"k{ci}_inverse_jacobian"] = g2.payload["inverse_jacobian"]
+        out[f"k{ci}_jxw"] = g2.payload["jxw"]
+        b = np.random.default_rng(0).uniform(-1.0, 1.0, h.n_dofs)
+        b[h.constrained_dofs] = 0.0
+        res = solve("combined_pcg", op, b, minv=op.compute_diagonal(), config=SolverConfig(fixed_iterations=40))
+        out[f"k{ci}_b"] = b
+        out[f"k{ci}_combined_pcg_hist"] = hist_array(res)
+        out[f"k{ci}_combined_pcg_x"] = res.x
+    np.savez_compressed(OUT / "curved.npz", **out)
+
+
+if __name__ == "__main__":
+    tables()
+    numbering()
+    apply_cases()
+    config1()
+    q5_small()
+    curved()
+    for f in sorted(OUT.glob("*.npz")):
+        print(f.name, f.stat().st_size)

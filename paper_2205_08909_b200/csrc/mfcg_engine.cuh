@@ -1,0 +1,469 @@
+// mfcg_engine.cuh -- host-side engine: owns device memory, launches the kernels,
+// runs the device-resident CG loops.  One Engine<P, T> per (degree, precision).
+#pragma once
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "mfcg_b200.h"
+#include "mfcg_kernels.cuh"
+
+namespace mfcg {
+
+void set_error(const std::string& msg);
+
+#define MFCG_CUDA(call)                                                                     \
+  do {                                                                                      \
+    cudaError_t err__ = (call);                                                             \
+    if (err__ != cudaSuccess) {                                                             \
+      set_error(std::string(#call) + ": " + cudaGetErrorString(err__));                     \
+      return err__ == cudaErrorMemoryAllocation ? MFCG_ENOMEM : MFCG_ECUDA;                 \
+    }                                                                                       \
+  } while (0)
+
+struct Ctx {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  void* nccl_comm = nullptr;
+  int rank = 0, n_ranks = 1;
+};
+
+// Everything mfcg_op_create derives that does not depend on the template arguments.
+struct OpCommon {
+  Ctx* ctx = nullptr;
+  BrickGrid grid{};
+  i64 n_cells = 0;
+  int p = 1, nq = 2, precision = 0, geometry = 0;
+  std::vector<double> S, D, xq, wq, glx, glw, glD;
+  double extents[3] = {1, 1, 1}, h[3] = {1, 1, 1}, deformation = 0.0;
+  i64 n_bricks = 0;
+  int* d_perm = nullptr;
+  i64* d_ent_start = nullptr;
+  unsigned char* d_mask = nullptr;
+  double* d_io = nullptr;       // fp64 staging in caller numbering
+  double* d_invdiag = nullptr;  // cached 1/diag, brick numbering, fp64
+  SolveState* d_state = nullptr;
+  SolveState* h_state = nullptr;  // pinned
+  int* d_flag = nullptr;
+};
+
+struct EngineBase {
+  virtual ~EngineBase() {}
+  virtual int apply(const double* src, double* dst, int location) = 0;
+  virtual int diagonal(double* out, int location) = 0;
+  virtual int solve(const mfcg_solve_args* a, mfcg_solve_result* r) = 0;
+  virtual void info(mfcg_op_info* out) = 0;
+};
+
+template <int P, typename T>
+class Engine : public EngineBase {
+ public:
+  static constexpr int N = P + 1;
+  static constexpr int VT = 256;  // threads of the vector kernels
+
+  explicit Engine(OpCommon* c) : c_(c) {}
+
+  ~Engine() override {
+    for (T** v : {&x_, &r_, &p_, &v_, &z_, &minv_}) if (*v) cudaFree(*v);
+    if (partials_a_) cudaFree(partials_a_);
+    if (partials_b_) cudaFree(partials_b_);
+    if (d_history_) cudaFree(d_history_);
+    for (cudaEvent_t e : events_) cudaEventDestroy(e);
+  }
+
+  int init() {
+    const double det = c_->h[0] * c_->h[1] * c_->h[2];
+    // M = S^T W S, K = D^T W D on [0,1] (tensor.py tables), scaled per direction
+    for (int i = 0; i < N; ++i)
+      for (int j = 0; j < N; ++j) {
+        double m = 0.0, k = 0.0;
+        for (int q = 0; q < c_->nq; ++q) {
+          m += c_->wq[q] * c_->S[q * N + i] * c_->S[q * N + j];
+          k += c_->wq[q] * c_->D[q * N + i] * c_->D[q * N + j];
+        }
+        tab_.M[i * N + j] = (T)m;
+        tab_.Kx[i * N + j] = (T)(k * det / (c_->h[0] * c_->h[0]));
+        tab_.Ky[i * N + j] = (T)(k * det / (c_->h[1] * c_->h[1]));
+        tab_.Kz[i * N + j] = (T)(k * det / (c_->h[2] * c_->h[2]));
+      }
+    // the mass factor of the cell volume is carried by the K's: A_e = sum_d Kd (x) M (x) M
+    smem_ = (int)Geo<P>::template smem_bytes<T>();
+    MFCG_CUDA(cudaFuncSetAttribute(k_brick<P, T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
+    MFCG_CUDA(cudaFuncSetAttribute(k_brick<P, T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
+    vgrid_ = c_->ctx->sm_count * 8;
+    const i64 rows = c_->n_bricks + vgrid_;
+    MFCG_CUDA(cudaMalloc(&partials_a_, sizeof(double) * 8 * rows));
+    MFCG_CUDA(cudaMalloc(&partials_b_, sizeof(double) * 8 * rows));
+    MFCG_CUDA(cudaMemsetAsync(partials_a_, 0, sizeof(double) * 8 * rows, stream()));
+    MFCG_CUDA(cudaMemsetAsync(partials_b_, 0, sizeof(double) * 8 * rows, stream()));
+    return MFCG_OK;
+  }
+
+  void info(mfcg_op_info* out) override {
+    out->n_dofs = c_->grid.n_dofs;
+    out->n_interior = c_->grid.n_int;
+    out->n_bricks = c_->n_bricks;
+    for (int d = 0; d < 3; ++d) out->brick[d] = c_->grid.B[d];
+    out->threads = Cfg<P>::THREADS;
+    out->smem_bytes = smem_;
+    out->geometry_bytes = 0;
+  }
+
+  int apply(const double* src, double* dst, int location) override {
+    int rc = ensure_vectors(false);
+    if (rc) return rc;
+    if ((rc = load_vec(src, location, p_))) return rc;
+    if ((rc = launch_apply(p_, v_))) return rc;
+    if ((rc = store_vec(v_, dst, location))) return rc;
+    MFCG_CUDA(cudaStreamSynchronize(stream()));
+    return MFCG_OK;
+  }
+
+  int diagonal(double* out, int location) override {
+    int rc = ensure_diagonal();
+    if (rc) return rc;
+    const i64 n = c_->grid.n_dofs;
+    double* target = location ? out : c_->d_io;
+    k_to_user_order<double><<<vgrid_, VT, 0, stream()>>>(n, c_->d_perm, c_->d_invdiag, target);
+    MFCG_CUDA(cudaGetLastError());
+    if (!location) MFCG_CUDA(cudaMemcpyAsync(out, c_->d_io, sizeof(double) * n, cudaMemcpyDeviceToHost, stream()));
+    MFCG_CUDA(cudaStreamSynchronize(stream()));
+    return MFCG_OK;
+  }
+
+  int solve(const mfcg_solve_args* a, mfcg_solve_result* res) override;
+
+ private:
+  cudaStream_t stream() const { return c_->ctx->stream; }
+
+  int ensure_vectors(bool all) {
+    const i64 n = c_->grid.n_dofs;
+    for (T** v : {&p_, &v_}) if (!*v) MFCG_CUDA(cudaMalloc(v, sizeof(T) * n));
+    if (all)
+      for (T** v : {&x_, &r_, &z_, &minv_}) if (!*v) MFCG_CUDA(cudaMalloc(v, sizeof(T) * n));
+    return MFCG_OK;
+  }
+
+  int ensure_diagonal() {
+    if (c_->d_invdiag) return MFCG_OK;
+    if (c_->geometry != MFCG_GEOM_AFFINE) {
+      set_error("Jacobi diagonal on curved geometry is not built yet in this round");
+      return MFCG_EUNSUPPORTED;
+    }
+    const i64 n = c_->grid.n_dofs;
+    double* diag = nullptr;
+    MFCG_CUDA(cudaMalloc(&diag, sizeof(double) * n));
+    MFCG_CUDA(cudaMemsetAsync(diag, 0, sizeof(double) * n, stream()));
+    DiagTables t{};
+    for (int i = 0; i < N; ++i) {
+      t.w[i] = c_->glw[i];
+      double dd = 0.0;
+      for (int q = 0; q < N; ++q) dd += c_->glw[q] * c_->glD[q * N + i] * c_->glD[q * N + i];
+      t.dd[i] = dd;
+    }
+    const double det = c_->h[0] * c_->h[1] * c_->h[2];
+    for (int d = 0; d < 3; ++d) t.g[d] = det / (c_->h[d] * c_->h[d]);
+    k_diag_affine<<<vgrid_, VT, 0, stream()>>>(c_->grid, t, c_->n_cells, diag);
+    MFCG_CUDA(cudaGetLastError());
+    MFCG_CUDA(cudaMemsetAsync(c_->d_flag, 0, sizeof(int), stream()));
+    k_diag_invert<<<vgrid_, VT, 0, stream()>>>(c_->grid, diag, c_->d_flag);
+    MFCG_CUDA(cudaGetLastError());
+    int flag = 0;
+    MFCG_CUDA(cudaMemcpyAsync(&flag, c_->d_flag, sizeof(int), cudaMemcpyDeviceToHost, stream()));
+    MFCG_CUDA(cudaStreamSynchronize(stream()));
+    if (flag) {
+      cudaFree(diag);
+      set_error("operator diagonal is not positive definite");
+      return MFCG_EINVAL;
+    }
+    c_->d_invdiag = diag;
+    return MFCG_OK;
+  }
+
+  // caller numbering (fp64, host or device) -> brick numbering (T, device)
+  int load_vec(const double* usr, int location, T* dev) {
+    const i64 n = c_->grid.n_dofs;
+    const double* from = usr;
+    if (!location) {
+      MFCG_CUDA(cudaMemcpyAsync(c_->d_io, usr, sizeof(double) * n, cudaMemcpyHostToDevice, stream()));
+      from = c_->d_io;
+    }
+    k_to_device_order<T><<<vgrid_, VT, 0, stream()>>>(n, c_->d_perm, from, dev);
+    MFCG_CUDA(cudaGetLastError());
+    ++launches_;
+    return MFCG_OK;
+  }
+
+  int store_vec(const T* dev, double* usr, int location) {
+    const i64 n = c_->grid.n_dofs;
+    double* target = location ? usr : c_->d_io;
+    k_to_user_order<T><<<vgrid_, VT, 0, stream()>>>(n, c_->d_perm, dev, target);
+    MFCG_CUDA(cudaGetLastError());
+    ++launches_;
+    if (!location) MFCG_CUDA(cudaMemcpyAsync(usr, c_->d_io, sizeof(double) * n, cudaMemcpyDeviceToHost, stream()));
+    return MFCG_OK;
+  }
+
+  int launch_brick(int mode, const T* src, T* pv, T* v, double* partials) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (time_kernels_) {
+      if (event_cursor_ + 2 > events_.size())
+        for (int i = 0; i < 2; ++i) {
+          cudaEvent_t e;
+          MFCG_CUDA(cudaEventCreate(&e));
+          events_.push_back(e);
+        }
+      e0 = events_[event_cursor_++];
+      e1 = events_[event_cursor_++];
+      MFCG_CUDA(cudaEventRecord(e0, stream()));
+    }
+    if (mode == 0)
+      k_brick<P, T, 0><<<(unsigned)c_->n_bricks, Cfg<P>::THREADS, smem_, stream()>>>(
+          c_->grid, tab_, src, nullptr, v, nullptr, nullptr, nullptr, nullptr, nullptr);
+    else
+      k_brick<P, T, 1><<<(unsigned)c_->n_bricks, Cfg<P>::THREADS, smem_, stream()>>>(
+          c_->grid, tab_, nullptr, pv, v, r_, x_, minv_, c_->d_state, partials);
+    MFCG_CUDA(cudaGetLastError());
+    if (time_kernels_) MFCG_CUDA(cudaEventRecord(e1, stream()));
+    ++launches_;
+    ++op_launches_;
+    return MFCG_OK;
+  }
+
+  // dst = A src in brick numbering
+  int launch_apply(const T* src, T* dst) {
+    if (c_->grid.n_dofs > c_->grid.n_int) {
+      k_surface_init<T><<<vgrid_, VT, 0, stream()>>>(c_->grid, src, dst);
+      MFCG_CUDA(cudaGetLastError());
+      ++launches_;
+    }
+    return launch_brick(0, src, nullptr, dst, nullptr);
+  }
+
+  int run_merged(const mfcg_solve_args* a, int limit);
+  int run_standard(const mfcg_solve_args* a, int limit, bool prec);
+
+  OpCommon* c_;
+  SepTables<T, N> tab_{};
+  int smem_ = 0, vgrid_ = 0;
+  T *x_ = nullptr, *r_ = nullptr, *p_ = nullptr, *v_ = nullptr, *z_ = nullptr, *minv_ = nullptr;
+  double *partials_a_ = nullptr, *partials_b_ = nullptr, *d_history_ = nullptr;
+  int history_cap_ = 0;
+  std::vector<cudaEvent_t> events_;
+  size_t event_cursor_ = 0;
+  bool time_kernels_ = false;
+  i64 launches_ = 0, op_launches_ = 0;
+};
+
+template <int P, typename T>
+int Engine<P, T>::run_merged(const mfcg_solve_args* a, int limit) {
+  const BrickGrid& g = c_->grid;
+  const i64 n = g.n_dofs, n_sh = g.n_dofs - g.n_int;
+  const bool fixed = a->fixed_iterations >= 0;
+  const int rows_fused = (int)c_->n_bricks + (n_sh > 0 ? vgrid_ : 0);
+  for (int it = 1; it <= limit; ++it) {
+    if (a->fused) {
+      if (n_sh > 0) {
+        k_pre<T><<<vgrid_, VT, 0, stream()>>>(g, g.n_int, n, 1, r_, p_, v_, x_, minv_, c_->d_state);
+        ++launches_;
+      }
+      int rc = launch_brick(1, nullptr, p_, v_, partials_a_);
+      if (rc) return rc;
+      if (n_sh > 0) {
+        k_post<T><<<vgrid_, VT, 0, stream()>>>(g.n_int, n, r_, p_, v_, minv_, c_->d_state,
+                                               partials_a_ + 8 * c_->n_bricks);
+        ++launches_;
+      }
+      k_scalar_merged<<<1, 256, 0, stream()>>>(partials_a_, rows_fused, c_->d_state, d_history_);
+      ++launches_;
+    } else {
+      // the paper's GPU scheme: pre, mat-vec and post as separate kernels
+      k_pre<T><<<vgrid_, VT, 0, stream()>>>(g, 0, n, 0, r_, p_, v_, x_, minv_, c_->d_state);
+      int rc = launch_apply(p_, v_);
+      if (rc) return rc;
+      k_post<T><<<vgrid_, VT, 0, stream()>>>(0, n, r_, p_, v_, minv_, c_->d_state, partials_a_);
+      k_scalar_merged<<<1, 256, 0, stream()>>>(partials_a_, vgrid_, c_->d_state, d_history_);
+      launches_ += 3;
+    }
+    MFCG_CUDA(cudaGetLastError());
+    if (!fixed && (it % 16 == 0)) {
+      MFCG_CUDA(cudaMemcpyAsync(c_->h_state, c_->d_state, sizeof(SolveState), cudaMemcpyDeviceToHost, stream()));
+      MFCG_CUDA(cudaStreamSynchronize(stream()));
+      if (!c_->h_state->active) break;
+    }
+  }
+  k_finalize_x<T><<<vgrid_, VT, 0, stream()>>>(n, x_, p_, r_, minv_, c_->d_state);
+  MFCG_CUDA(cudaGetLastError());
+  ++launches_;
+  return MFCG_OK;
+}
+
+template <int P, typename T>
+int Engine<P, T>::run_standard(const mfcg_solve_args* a, int limit, bool prec) {
+  const BrickGrid& g = c_->grid;
+  const i64 n = g.n_dofs;
+  const bool fixed = a->fixed_iterations >= 0;
+  T* z = prec ? z_ : r_;
+  // v_ holds b in brick numbering on entry
+  k_std_init<T><<<vgrid_, VT, 0, stream()>>>(n, v_, prec ? minv_ : nullptr, r_, z_, p_, x_, partials_a_);
+  k_std_init_scalar<<<1, 256, 0, stream()>>>(partials_a_, vgrid_, c_->d_state);
+  launches_ += 2;
+  MFCG_CUDA(cudaGetLastError());
+  for (int it = 1; it <= limit; ++it) {
+    int rc = launch_apply(p_, v_);
+    if (rc) return rc;
+    k_dot<T><<<vgrid_, VT, 0, stream()>>>(n, p_, v_, c_->d_state, partials_a_);
+    k_std_alpha<<<1, 256, 0, stream()>>>(partials_a_, vgrid_, c_->d_state);
+    k_std_axpy<T><<<vgrid_, VT, 0, stream()>>>(n, x_, p_, 1.0, c_->d_state);
+    k_std_axpy<T><<<vgrid_, VT, 0, stream()>>>(n, r_, v_, -1.0, c_->d_state);
+    k_dot<T><<<vgrid_, VT, 0, stream()>>>(n, r_, r_, c_->d_state, partials_a_);
+    launches_ += 5;
+    if (prec) {
+      k_std_prec<T><<<vgrid_, VT, 0, stream()>>>(n, z_, minv_, r_, c_->d_state);
+      k_dot<T><<<vgrid_, VT, 0, stream()>>>(n, r_, z_, c_->d_state, partials_b_);
+      launches_ += 2;
+    }
+    k_std_beta<<<1, 256, 0, stream()>>>(partials_a_, prec ? partials_b_ : nullptr, vgrid_, c_->d_state, d_history_);
+    k_std_update_p<T><<<vgrid_, VT, 0, stream()>>>(n, p_, z, c_->d_state);
+    launches_ += 2;
+    MFCG_CUDA(cudaGetLastError());
+    if (!fixed && (it % 16 == 0)) {
+      MFCG_CUDA(cudaMemcpyAsync(c_->h_state, c_->d_state, sizeof(SolveState), cudaMemcpyDeviceToHost, stream()));
+      MFCG_CUDA(cudaStreamSynchronize(stream()));
+      if (!c_->h_state->active) break;
+    }
+  }
+  return MFCG_OK;
+}
+
+template <int P, typename T>
+int Engine<P, T>::solve(const mfcg_solve_args* a, mfcg_solve_result* res) {
+  std::memset(res, 0, sizeof(*res));
+  const BrickGrid& g = c_->grid;
+  const i64 n = g.n_dofs;
+  const bool merged = a->variant == MFCG_COMBINED_CG || a->variant == MFCG_COMBINED_PCG;
+  const bool prec = a->variant == MFCG_PCG || a->variant == MFCG_COMBINED_PCG;
+  if (a->variant < 0 || a->variant > 3) { set_error("unknown solver variant"); return MFCG_EINVAL; }
+  if (!a->b || !a->x) { set_error("b and x must not be NULL"); return MFCG_EINVAL; }
+  if (a->tolerance <= 0) { set_error("tolerance must be positive"); return MFCG_EINVAL; }
+  if (a->max_iterations < 1) { set_error("max_iterations must be at least 1"); return MFCG_EINVAL; }
+  const bool fixed = a->fixed_iterations >= 0;
+  // solvers.py:210: `limit = cfg.fixed_iterations or cfg.max_iterations` (0 falls through)
+  const int limit = a->fixed_iterations > 0 ? a->fixed_iterations : a->max_iterations;
+  int rc = ensure_vectors(true);
+  if (rc) return rc;
+  if (history_cap_ < limit) {
+    if (d_history_) cudaFree(d_history_);
+    MFCG_CUDA(cudaMalloc(&d_history_, sizeof(double) * 4 * (size_t)limit));
+    history_cap_ = limit;
+  }
+  launches_ = op_launches_ = 0;
+  time_kernels_ = a->time_kernels != 0;
+  event_cursor_ = 0;
+
+  cudaEvent_t t0, t1;
+  MFCG_CUDA(cudaEventCreate(&t0));
+  MFCG_CUDA(cudaEventCreate(&t1));
+  MFCG_CUDA(cudaEventRecord(t0, stream()));
+
+  // right-hand side: merged variants start with r = b, the standard ones stage b in v
+  if ((rc = load_vec(a->b, a->location, merged ? r_ : v_))) return rc;
+  if (prec) {
+    if (a->inv_diag) {
+      if ((rc = load_vec(a->inv_diag, a->location, minv_))) return rc;
+    } else {
+      if ((rc = ensure_diagonal())) return rc;
+      k_convert<T, double><<<vgrid_, VT, 0, stream()>>>(n, c_->d_invdiag, minv_);
+      ++launches_;
+    }
+  } else if (merged) {
+    k_fill<T><<<vgrid_, VT, 0, stream()>>>(n, minv_, (T)1);
+    ++launches_;
+  }
+  const T* bvec = merged ? r_ : v_;
+  k_dot<T><<<vgrid_, VT, 0, stream()>>>(n, bvec, bvec, nullptr, partials_a_);
+  ++launches_;
+  MFCG_CUDA(cudaGetLastError());
+  std::vector<double> hp(8 * (size_t)vgrid_);
+  MFCG_CUDA(cudaMemcpyAsync(hp.data(), partials_a_, sizeof(double) * hp.size(), cudaMemcpyDeviceToHost, stream()));
+  MFCG_CUDA(cudaStreamSynchronize(stream()));
+  double bb = 0.0;
+  for (int i = 0; i < vgrid_; ++i) bb += hp[8 * (size_t)i];
+  const double bnorm = std::sqrt(bb);
+  res->bnorm = bnorm;
+  if (bnorm == 0.0) {  // solvers.py:156-157, 191-192: zero rhs -> x = 0, 0 iterations, converged
+    MFCG_CUDA(cudaMemsetAsync(x_, 0, sizeof(T) * n, stream()));
+    if ((rc = store_vec(x_, a->x, a->location))) return rc;
+    MFCG_CUDA(cudaStreamSynchronize(stream()));
+    res->converged = 1;
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    return MFCG_OK;
+  }
+  SolveState s0;
+  std::memset(&s0, 0, sizeof(s0));
+  s0.active = 1;
+  s0.fixed = fixed ? 1 : 0;
+  s0.force_x = a->force_x_updates ? 1 : 0;
+  s0.has_prec = prec ? 1 : 0;
+  s0.limit = limit;
+  s0.bnorm = bnorm;
+  s0.tol = a->tolerance;
+  s0.residual = 1.0;  // ||r0|| / ||b|| with r0 = b
+  *c_->h_state = s0;
+  MFCG_CUDA(cudaMemcpyAsync(c_->d_state, c_->h_state, sizeof(SolveState), cudaMemcpyHostToDevice, stream()));
+  if (merged) {
+    MFCG_CUDA(cudaMemsetAsync(x_, 0, sizeof(T) * n, stream()));
+    MFCG_CUDA(cudaMemsetAsync(p_, 0, sizeof(T) * n, stream()));
+    MFCG_CUDA(cudaMemsetAsync(v_, 0, sizeof(T) * n, stream()));
+    rc = run_merged(a, limit);
+  } else {
+    rc = run_standard(a, limit, prec);
+  }
+  if (rc) return rc;
+  if ((rc = store_vec(x_, a->x, a->location))) return rc;
+  MFCG_CUDA(cudaEventRecord(t1, stream()));
+  MFCG_CUDA(cudaMemcpyAsync(c_->h_state, c_->d_state, sizeof(SolveState), cudaMemcpyDeviceToHost, stream()));
+  MFCG_CUDA(cudaStreamSynchronize(stream()));
+  const SolveState& s = *c_->h_state;
+  float ms = 0.f;
+  MFCG_CUDA(cudaEventElapsedTime(&ms, t0, t1));
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  res->solve_ms = ms;
+  if (time_kernels_) {
+    double acc = 0.0;
+    for (size_t i = 0; i + 1 < event_cursor_; i += 2) {
+      float m = 0.f;
+      MFCG_CUDA(cudaEventElapsedTime(&m, events_[i], events_[i + 1]));
+      acc += m;
+    }
+    res->operator_ms = acc;
+  }
+  res->kernel_launches = launches_;
+  res->operator_launches = op_launches_;
+  res->iterations = s.k;
+  res->matvecs = (int)op_launches_;
+  res->residual = s.residual;
+  res->breakdown = s.breakdown;
+  res->breakdown_iteration = s.breakdown_iteration;
+  res->breakdown_value = s.breakdown_value;
+  res->converged = fixed ? (s.residual < a->tolerance) : s.converged;
+  if (a->history && s.k > 0)
+    MFCG_CUDA(cudaMemcpy(a->history, d_history_, sizeof(double) * 4 * (size_t)s.k, cudaMemcpyDeviceToHost));
+  if (s.breakdown) {
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), "breakdown code %d: value %.3e <= 0 at iteration %d", s.breakdown,
+                  s.breakdown_value, s.breakdown_iteration);
+    set_error(buf);
+    return MFCG_EBREAKDOWN;
+  }
+  return MFCG_OK;
+}
+
+EngineBase* make_engine(OpCommon* c);  // dispatch over (degree, precision), mfcg_b200.cu
+
+}  // namespace mfcg

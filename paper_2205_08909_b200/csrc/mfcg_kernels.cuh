@@ -1,0 +1,720 @@
+// mfcg_kernels.cuh -- sm_100a kernels of the matrix-free CG hot path.
+//
+// Reference semantics (file:line relative to /root/reference/pkg/src/mfcg):
+//   cell Laplacian          operator.py:253-281 + tensor.py:313-370
+//   gather/scatter, BCs     operator.py:338-360
+//   merged CG pre/post      solvers.py:660-698, fused_reductions solvers.py:112-127
+//   scalar recurrences      solvers.py:706-764
+//   standard (P)CG          solvers.py:183-340
+//   Jacobi diagonal         operator.py:380-418
+//
+// Data layout.  The mesh is cut into bricks of
+// Bx x By x Bz cells; one thread block owns one brick and marches through it
+// cell layer by cell layer.  DoF vectors live in "brick numbering": the DoFs
+// strictly inside a brick form one contiguous block (x fastest), all DoFs on
+// brick faces/edges/corners ("shared") follow behind all interiors, entity by
+// entity.  Interior DoFs are read once and written once per merged-CG
+// iteration without leaving the SM; shared DoFs (about 12 % at p = 5) take the
+// pre -> atomic accumulate -> post route through the small k_pre/k_post kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mfcg {
+
+typedef long long i64;
+
+struct BrickGrid {
+  int p;
+  int cells[3];   // cells of this rank's mesh (slab)
+  int B[3];       // nominal cells per brick
+  int mb[3];      // bricks per direction
+  i64 n_dofs;
+  i64 n_int;      // brick-interior DoFs occupy [0, n_int)
+  const i64* ent_start;        // start of every macro entity, [2mbz+1][2mby+1][2mbx+1]
+  const unsigned char* mask;   // constrained flag of shared DoF n_int + s
+};
+
+// Device-resident solver state: the iteration loop never synchronises with
+// the host; scalar kernels advance this struct (solvers.py:706-764).
+struct SolveState {
+  double am1, bm1, am2, bm2;  // alpha/beta of the two previous iterations
+  double xc1, xc2;            // x catch-up coefficients for the next pre
+  int xmode;                  // 0 none, 1 x += xc1 p, 2 x += xc1 p + xc2 (p - M r)
+  int active;                 // 0 once converged / broken down: kernels return at once
+  int k;                      // iterations completed
+  int stagnant, converged, breakdown, breakdown_iteration;
+  int fixed, force_x, has_prec, limit;
+  double breakdown_value;
+  double residual, bnorm, tol;
+  double gamma, alpha, beta;  // standard (P)CG scalars
+};
+
+template <int P> struct Cfg;
+#define MFCG_CFG(P_, B_, T_, MB_) \
+  template <> struct Cfg<P_> { static constexpr int BX = B_, BY = B_, THREADS = T_, MINB = MB_; };
+MFCG_CFG(1, 16, 512, 2)
+MFCG_CFG(2, 10, 320, 2)
+MFCG_CFG(3, 6, 288, 2)
+MFCG_CFG(4, 5, 320, 2)
+MFCG_CFG(5, 4, 288, 2)
+MFCG_CFG(6, 3, 224, 2)
+MFCG_CFG(7, 2, 256, 2)
+MFCG_CFG(8, 2, 192, 2)
+
+template <int P> struct Geo {
+  static constexpr int N = P + 1;
+  static constexpr int RS = (N % 2 == 0) ? N + 1 : N;  // odd row stride: conflict-free 64-bit columns
+  static constexpr int TILE = N * N * RS;
+  static constexpr int NCELL = Cfg<P>::BX * Cfg<P>::BY;
+  static constexpr int WX = P * Cfg<P>::BX + 1;         // window row stride (odd for every Cfg)
+  static constexpr int PLANE = WX * (P * Cfg<P>::BY + 1);
+  template <typename T> __host__ __device__ static constexpr size_t red_offset() {
+    return (256 + sizeof(T) * (size_t)(N * PLANE + PLANE + 2 * NCELL * TILE) + 15) & ~(size_t)15;
+  }
+  template <typename T> __host__ __device__ static constexpr size_t smem_bytes() { return red_offset<T>() + 8 * 7 * 32; }
+};
+
+// 1D matrices of the separable (Cartesian/affine) cell operator
+//   A_e = Kx (x) M (x) M + M (x) Ky (x) M + M (x) M (x) Kz,
+// M = S^T W S, Kd = (det J / h_d^2) D^T W D, rows = output index.  Passed by
+// value: kernel parameters sit in the constant bank, so every entry is an
+// immediate c[0x0][..] operand of the DFMA.
+template <typename T, int N> struct SepTables {
+  T M[N * N], Kx[N * N], Ky[N * N], Kz[N * N];
+};
+
+__device__ __forceinline__ int brick_cells(const BrickGrid& g, int d, int m) {
+  int r = g.cells[d] - m * g.B[d];
+  return r < g.B[d] ? r : g.B[d];
+}
+
+__device__ __forceinline__ void warp_reduce7(double* s) {
+#pragma unroll
+  for (int q = 0; q < 7; ++q)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
+}
+
+// Block-level reduction of seven sums; result row written by thread 0.
+// red: >= 7*32 doubles of shared memory.
+__device__ __forceinline__ void block_reduce7_store(double* s, double* red, double* out_row) {
+  warp_reduce7(s);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < 7; ++q) red[w * 7 + q] = s[q];
+  __syncthreads();
+  if (threadIdx.x < 7) {
+    double acc = 0.0;
+    for (int i = 0; i < nw; ++i) acc += red[i * 7 + threadIdx.x];
+    out_row[threadIdx.x] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// The brick kernel.  MODE 0: dst = A src (operator.py:285-360).
+// MODE 1: one merged-CG iteration on brick-interior DoFs (solvers.py:660-704):
+// pre on load, cell work, post on the finished values; shared DoFs have been
+// pre-updated by k_pre and receive atomic contributions.
+template <int P, typename T, int MODE>
+__global__ void __launch_bounds__(Cfg<P>::THREADS, Cfg<P>::MINB)
+k_brick(BrickGrid g, SepTables<T, P + 1> tab, const T* __restrict__ src, T* __restrict__ Pv,
+        T* __restrict__ V, T* __restrict__ R, T* __restrict__ X, const T* __restrict__ Minv,
+        const SolveState* __restrict__ st, double* __restrict__ partials) {
+  constexpr int N = P + 1, RS = Geo<P>::RS, TILE = Geo<P>::TILE, WX = Geo<P>::WX,
+                PLANE = Geo<P>::PLANE, NCELL = Geo<P>::NCELL, NT = Cfg<P>::THREADS;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  i64* st27 = reinterpret_cast<i64*>(smem_raw);
+  T* Pw = reinterpret_cast<T*>(smem_raw + 256);
+  T* carry = Pw + N * PLANE;
+  T* A = carry + PLANE;
+  T* Bs = A + NCELL * TILE;
+  constexpr size_t RED_OFF = Geo<P>::template red_offset<T>();
+  double* red = reinterpret_cast<double*>(smem_raw + RED_OFF);
+
+  const int tid = threadIdx.x;
+  T am1 = 0, bm1 = 0, xc1 = 0, xc2 = 0;
+  int xmode = 0;
+  if (MODE == 1) {
+    if (!st->active) return;
+    am1 = (T)st->am1; bm1 = (T)st->bm1; xc1 = (T)st->xc1; xc2 = (T)st->xc2; xmode = st->xmode;
+  }
+
+  const int b = blockIdx.x;
+  const int mx = b % g.mb[0];
+  const int my = (b / g.mb[0]) % g.mb[1];
+  const int mz = b / (g.mb[0] * g.mb[1]);
+  const int bcx = brick_cells(g, 0, mx), bcy = brick_cells(g, 1, my), bcz = brick_cells(g, 2, mz);
+  const int Lx = P * bcx, Ly = P * bcy, Lz = P * bcz;
+  if (tid < 27) {
+    const int ex = tid % 3, ey = (tid / 3) % 3, ez = tid / 9;
+    st27[tid] = g.ent_start[((i64)(2 * mz + ez) * (2 * g.mb[1] + 1) + (2 * my + ey)) * (2 * g.mb[0] + 1) + 2 * mx + ex];
+  }
+  for (int i = tid; i < PLANE; i += NT) carry[i] = (T)0;
+  __syncthreads();
+
+  const int fw = Lx + 1, fp = fw * (Ly + 1);
+  const unsigned fw_magic = (65536u + fw - 1) / fw;
+  const int ncell = bcx * bcy;
+  const unsigned bcx_magic = (65536u + bcx - 1) / bcx;
+  const i64 n_int = g.n_int;
+  double s[7] = {0, 0, 0, 0, 0, 0, 0};
+
+  for (int kz = 0; kz < bcz; ++kz) {
+    const int k0 = kz == 0 ? 0 : 1;
+    // ---- load the layer's lattice planes (pre fused for interior DoFs)
+    for (int rem = tid; rem < fp; rem += NT) {
+      const int j = (int)(((unsigned)rem * fw_magic) >> 16);
+      const int i = rem - j * fw;
+      const int ex = i == 0 ? 0 : (i == Lx ? 2 : 1), ey = j == 0 ? 0 : (j == Ly ? 2 : 1);
+      const int ox = ex == 1 ? i - 1 : 0, oy = ey == 1 ? j - 1 : 0;
+      const int lx = ex == 1 ? Lx - 1 : 1, ly = ey == 1 ? Ly - 1 : 1;
+      const bool edge = (ex != 1) || (ey != 1);
+#pragma unroll
+      for (int k = 0; k <= P; ++k) {
+        if (k < k0) continue;
+        const int K = kz * P + k;
+        const int ez = K == 0 ? 0 : (K == Lz ? 2 : 1);
+        const int oz = ez == 1 ? K - 1 : 0;
+        const i64 gi = st27[ex + 3 * ey + 9 * ez] + ox + (i64)lx * (oy + ly * oz);
+        const bool shared = edge || ez != 1;
+        T val;
+        if (MODE == 0) {
+          val = src[gi];
+          if (shared && g.mask[gi - n_int]) val = (T)0;
+        } else {
+          if (!shared) {
+            T r = R[gi], v = V[gi], p = Pv[gi];
+            const T m = Minv[gi];
+            if (xmode) {
+              T x = X[gi];
+              if (xmode == 2) x += xc1 * p + xc2 * (p - m * r);
+              else x += xc1 * p;
+              X[gi] = x;
+            }
+            r -= am1 * v;
+            p = m * r + bm1 * p;
+            R[gi] = r;
+            Pv[gi] = p;
+            val = p;
+          } else {
+            val = g.mask[gi - n_int] ? (T)0 : Pv[gi];
+          }
+        }
+        Pw[k * PLANE + j * WX + i] = val;
+      }
+    }
+    __syncthreads();
+
+    // ---- x sweep: a = M u, b = Kx u along every x line of every cell
+    for (int w = tid; w < ncell * N * N; w += NT) {
+      const int cell = w / (N * N);
+      const int rr = w - cell * (N * N);
+      const int k = rr / N, j = rr - k * N;
+      const int cy = (int)(((unsigned)cell * bcx_magic) >> 16);
+      const int cx = cell - cy * bcx;
+      const T* row = Pw + k * PLANE + (cy * P + j) * WX + cx * P;
+      T u[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) u[i] = row[i];
+      T* ao = A + cell * TILE + (k * N + j) * RS;
+      T* bo = Bs + cell * TILE + (k * N + j) * RS;
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        T a = 0, bb = 0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          a += tab.M[q * N + i] * u[i];
+          bb += tab.Kx[q * N + i] * u[i];
+        }
+        ao[q] = a;
+        bo[q] = bb;
+      }
+    }
+    __syncthreads();
+
+    // ---- y sweep (in place): c = M a, de = Ky a + M b
+    for (int w = tid; w < ncell * N * N; w += NT) {
+      const int cell = w / (N * N);
+      const int rr = w - cell * (N * N);
+      const int k = rr / N, i = rr - k * N;
+      T* ac = A + cell * TILE + k * N * RS + i;
+      T* bc = Bs + cell * TILE + k * N * RS + i;
+      T a[N], bb[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) { a[j] = ac[j * RS]; bb[j] = bc[j * RS]; }
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        T c = 0, de = 0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          c += tab.M[q * N + j] * a[j];
+          de += tab.Ky[q * N + j] * a[j];
+        }
+#pragma unroll
+        for (int j = 0; j < N; ++j) de += tab.M[q * N + j] * bb[j];
+        ac[q * RS] = c;
+        bc[q * RS] = de;
+      }
+    }
+    __syncthreads();
+
+    // ---- z sweep: out = M de + Kz c, written over c
+    for (int w = tid; w < ncell * N * N; w += NT) {
+      const int cell = w / (N * N);
+      const int rr = w - cell * (N * N);
+      const int j = rr / N, i = rr - j * N;
+      T* ac = A + cell * TILE + j * RS + i;
+      const T* bc = Bs + cell * TILE + j * RS + i;
+      T c[N], de[N];
+#pragma unroll
+      for (int k = 0; k < N; ++k) { c[k] = ac[k * N * RS]; de[k] = bc[k * N * RS]; }
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        T o = 0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) o += tab.M[q * N + k] * de[k];
+#pragma unroll
+        for (int k = 0; k < N; ++k) o += tab.Kz[q * N + k] * c[k];
+        ac[q * N * RS] = o;
+      }
+    }
+    __syncthreads();
+
+    // ---- gather the cells' contributions per lattice point, finish the planes
+    for (int rem = tid; rem < fp; rem += NT) {
+      const int j = (int)(((unsigned)rem * fw_magic) >> 16);
+      const int i = rem - j * fw;
+      const int ex = i == 0 ? 0 : (i == Lx ? 2 : 1), ey = j == 0 ? 0 : (j == Ly ? 2 : 1);
+      const int ox = ex == 1 ? i - 1 : 0, oy = ey == 1 ? j - 1 : 0;
+      const int lx = ex == 1 ? Lx - 1 : 1, ly = ey == 1 ? Ly - 1 : 1;
+      const bool edge = (ex != 1) || (ey != 1);
+      int cx1 = i / P;
+      const int ix1 = i - cx1 * P;
+      const int cx0 = (ix1 == 0 && cx1 > 0) ? cx1 - 1 : -1;
+      if (cx1 >= bcx) cx1 = -1;
+      int cy1 = j / P;
+      const int iy1 = j - cy1 * P;
+      const int cy0 = (iy1 == 0 && cy1 > 0) ? cy1 - 1 : -1;
+      if (cy1 >= bcy) cy1 = -1;
+      // offsets of the (up to four) cell-tile entries holding this point
+      const int o11 = (cy1 >= 0 && cx1 >= 0) ? (cy1 * bcx + cx1) * TILE + iy1 * RS + ix1 : -1;
+      const int o10 = (cy1 >= 0 && cx0 >= 0) ? (cy1 * bcx + cx0) * TILE + iy1 * RS + P : -1;
+      const int o01 = (cy0 >= 0 && cx1 >= 0) ? (cy0 * bcx + cx1) * TILE + P * RS + ix1 : -1;
+      const int o00 = (cy0 >= 0 && cx0 >= 0) ? (cy0 * bcx + cx0) * TILE + P * RS + P : -1;
+#pragma unroll
+      for (int k = 0; k <= P; ++k) {
+        T sum = 0;
+        if (o00 >= 0) sum += A[o00 + k * N * RS];
+        if (o01 >= 0) sum += A[o01 + k * N * RS];
+        if (o10 >= 0) sum += A[o10 + k * N * RS];
+        if (o11 >= 0) sum += A[o11 + k * N * RS];
+        if (k == 0) sum += carry[j * WX + i];
+        if (k == P && kz < bcz - 1) {
+          carry[j * WX + i] = sum;
+          Pw[j * WX + i] = Pw[P * PLANE + j * WX + i];
+          continue;
+        }
+        const int K = kz * P + k;
+        const int ez = K == 0 ? 0 : (K == Lz ? 2 : 1);
+        const int oz = ez == 1 ? K - 1 : 0;
+        const i64 gi = st27[ex + 3 * ey + 9 * ez] + ox + (i64)lx * (oy + ly * oz);
+        if (!(edge || ez != 1)) {
+          V[gi] = sum;
+          if (MODE == 1) {
+            const double r = (double)R[gi], m = (double)Minv[gi];
+            const double p = (double)Pw[k * PLANE + j * WX + i], v = (double)sum;
+            const double mr = m * r, mv = m * v;
+            s[0] += r * r; s[1] += p * v; s[2] += r * v; s[3] += v * v;
+            s[4] += r * mr; s[5] += r * mv; s[6] += v * mv;
+          }
+        } else if (!g.mask[gi - n_int]) {
+          atomicAdd(&V[gi], sum);
+        }
+      }
+    }
+    // next layer's loads are ordered after this gather by the barrier that
+    // follows them; Pw[1..P] is only rewritten by the thread that just read it
+  }
+  if (MODE == 1) block_reduce7_store(s, red, partials + (i64)blockIdx.x * 8);
+}
+
+// ---------------------------------------------------------------------------
+// Range kernels over [lo, hi) in brick numbering.
+
+// dst[i] = constrained ? src[i] : 0 on the shared range (operator.py:334-335, 359-360)
+template <typename T>
+__global__ void k_surface_init(BrickGrid g, const T* __restrict__ src, T* __restrict__ dst) {
+  const i64 n_sh = g.n_dofs - g.n_int;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n_sh; i += (i64)gridDim.x * blockDim.x)
+    dst[g.n_int + i] = g.mask[i] ? src[g.n_int + i] : (T)0;
+}
+
+// merged-CG "pre" (solvers.py:660-690); with init_v also resets v for the
+// atomic accumulation: constrained rows are identity, v_c = p_c.
+template <typename T>
+__global__ void k_pre(BrickGrid g, i64 lo, i64 hi, int init_v, T* __restrict__ R, T* __restrict__ Pv,
+                      T* __restrict__ V, T* __restrict__ X, const T* __restrict__ Minv,
+                      const SolveState* __restrict__ st) {
+  if (!st->active) return;
+  const T am1 = (T)st->am1, bm1 = (T)st->bm1, xc1 = (T)st->xc1, xc2 = (T)st->xc2;
+  const int xmode = st->xmode;
+  for (i64 i = lo + blockIdx.x * (i64)blockDim.x + threadIdx.x; i < hi; i += (i64)gridDim.x * blockDim.x) {
+    T r = R[i], p = Pv[i];
+    const T v = V[i], m = Minv[i];
+    if (xmode) {
+      T x = X[i];
+      if (xmode == 2) x += xc1 * p + xc2 * (p - m * r);
+      else x += xc1 * p;
+      X[i] = x;
+    }
+    r -= am1 * v;
+    p = m * r + bm1 * p;
+    R[i] = r;
+    Pv[i] = p;
+    if (init_v) V[i] = (i >= g.n_int && g.mask[i - g.n_int]) ? p : (T)0;
+  }
+}
+
+// merged-CG "post": the seven sums (solvers.py:112-127, 692-698)
+template <typename T>
+__global__ void k_post(i64 lo, i64 hi, const T* __restrict__ R, const T* __restrict__ Pv,
+                       const T* __restrict__ V, const T* __restrict__ Minv,
+                       const SolveState* __restrict__ st, double* __restrict__ partials) {
+  __shared__ double red[7 * 32];
+  if (!st->active) return;
+  double s[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (i64 i = lo + blockIdx.x * (i64)blockDim.x + threadIdx.x; i < hi; i += (i64)gridDim.x * blockDim.x) {
+    const double r = (double)R[i], p = (double)Pv[i], v = (double)V[i], m = (double)Minv[i];
+    const double mr = m * r, mv = m * v;
+    s[0] += r * r; s[1] += p * v; s[2] += r * v; s[3] += v * v;
+    s[4] += r * mr; s[5] += r * mv; s[6] += v * mv;
+  }
+  block_reduce7_store(s, red, partials + (i64)blockIdx.x * 8);
+}
+
+// x catch-up after the loop (solvers.py:771-782)
+template <typename T>
+__global__ void k_finalize_x(i64 n, T* __restrict__ X, const T* __restrict__ Pv, const T* __restrict__ R,
+                             const T* __restrict__ Minv, const SolveState* __restrict__ st) {
+  const int k = st->k;
+  if (k <= 0) return;
+  const T a1 = (T)st->am1;
+  const bool simple = st->force_x || (k & 1) || st->am2 == 0.0 || st->bm2 == 0.0;
+  const T c2 = simple ? (T)0 : (T)(st->am2 / st->bm2);
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const T p = Pv[i];
+    X[i] += simple ? a1 * p : a1 * p + c2 * (p - Minv[i] * R[i]);
+  }
+}
+
+// Deterministic sum of `rows` partial rows (stride 8) into out[0..cols)
+__device__ __forceinline__ void reduce_rows(const double* __restrict__ partials, int rows, int cols, double* out,
+                                            double* red /* blockDim.x * cols? no: 8*32 */) {
+  double s[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (int r = threadIdx.x; r < rows; r += blockDim.x)
+    for (int q = 0; q < cols; ++q) s[q] += partials[(i64)r * 8 + q];
+  warp_reduce7(s);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  if (lane == 0)
+    for (int q = 0; q < 7; ++q) red[w * 7 + q] = s[q];
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int q = 0; q < cols; ++q) {
+      double acc = 0.0;
+      for (int i = 0; i < nw; ++i) acc += red[i * 7 + q];
+      out[q] = acc;
+    }
+  __syncthreads();
+}
+
+// Scalar step of the merged iteration (solvers.py:706-764), one block.
+static __global__ void k_scalar_merged(const double* __restrict__ partials, int rows, SolveState* st,
+                                double* __restrict__ history) {
+  __shared__ double red[7 * 32];
+  __shared__ double sums[8];
+  if (!st->active) return;
+  reduce_rows(partials, rows, 7, sums, red);
+  if (threadIdx.x != 0) return;
+  const double gamma = sums[0], a = sums[1], bb = sums[2], cc = sums[3], d = sums[4], e = sums[5], f = sums[6];
+  const int k = st->k + 1;
+  const bool fixed = st->fixed != 0;
+  double alpha = 0.0, beta = 0.0, residual = st->residual;
+  bool stop = false;
+  if (st->stagnant) {
+    residual = sqrt(gamma) / st->bnorm;
+  } else if (gamma == 0.0) {
+    residual = 0.0;
+    if (fixed) st->stagnant = 1;
+    else { st->converged = 1; stop = true; }
+  } else if (st->has_prec && d <= 0.0) {
+    st->breakdown = 2; st->breakdown_value = d; st->breakdown_iteration = k; st->active = 0;
+    return;
+  } else if (a <= 0.0) {
+    if (fixed && residual < st->tol) st->stagnant = 1;
+    else { st->breakdown = 1; st->breakdown_value = a; st->breakdown_iteration = k; st->active = 0; return; }
+  } else {
+    alpha = d / a;
+    beta = (d - 2.0 * alpha * e + alpha * alpha * f) / d;
+    const double stop_sq = gamma - 2.0 * alpha * bb + alpha * alpha * cc;
+    residual = sqrt(stop_sq > 0.0 ? stop_sq : 0.0) / st->bnorm;
+    if (beta <= 0.0 && fixed) {
+      if (residual < st->tol) st->stagnant = 1;
+      else { st->breakdown = 3; st->breakdown_value = beta; st->breakdown_iteration = k; st->active = 0; return; }
+    }
+  }
+  history[(i64)(k - 1) * 4 + 0] = alpha;
+  history[(i64)(k - 1) * 4 + 1] = beta;
+  history[(i64)(k - 1) * 4 + 2] = gamma;
+  history[(i64)(k - 1) * 4 + 3] = residual;
+  st->am2 = st->am1; st->bm2 = st->bm1;
+  st->am1 = alpha; st->bm1 = beta;
+  st->k = k;
+  st->residual = residual;
+  if (!fixed && residual < st->tol) { st->converged = 1; stop = true; }
+  if (stop || k >= st->limit) st->active = 0;
+  // x catch-up of the next pre (iteration k+1), solvers.py:661-677
+  const int kn = k + 1;
+  const bool live = st->am1 != 0.0 || st->am2 != 0.0;
+  int xmode = 0;
+  if (kn > 1 && live && (st->force_x || (kn & 1))) {
+    if (st->force_x) xmode = 1;
+    else if (st->am2 != 0.0 && st->bm2 != 0.0) { xmode = 2; st->xc2 = st->am2 / st->bm2; }
+    else xmode = 1;
+    st->xc1 = st->am1;
+  }
+  st->xmode = xmode;
+}
+
+// ---------------------------------------------------------------------------
+// Standard (unfused) CG / PCG: one kernel per vector region of the reference
+// (solvers.py:296-336), scalars stay on the device.
+
+template <typename T>
+__global__ void k_dot(i64 n, const T* __restrict__ a, const T* __restrict__ b, const SolveState* st,
+                      double* __restrict__ partials) {
+  __shared__ double red[7 * 32];
+  if (st && !st->active) return;
+  double s[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    s[0] += (double)a[i] * (double)b[i];
+  block_reduce7_store(s, red, partials + (i64)blockIdx.x * 8);
+}
+
+// r = b, z = M r, p = z (or p = r), partial sums of r.z (col 0) and r.r (col 1)
+template <typename T>
+__global__ void k_std_init(i64 n, const T* __restrict__ B, const T* __restrict__ Minv, T* __restrict__ R,
+                           T* __restrict__ Z, T* __restrict__ Pv, T* __restrict__ X, double* __restrict__ partials) {
+  __shared__ double red[7 * 32];
+  double s[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const T r = B[i];
+    const T z = Minv ? Minv[i] * r : r;
+    R[i] = r;
+    if (Minv) Z[i] = z;
+    Pv[i] = z;
+    X[i] = (T)0;
+    s[0] += (double)r * (double)z;
+    s[1] += (double)r * (double)r;
+  }
+  block_reduce7_store(s, red, partials + (i64)blockIdx.x * 8);
+}
+
+static __global__ void k_std_init_scalar(const double* __restrict__ partials, int rows, SolveState* st) {
+  __shared__ double red[7 * 32];
+  __shared__ double sums[8];
+  reduce_rows(partials, rows, 2, sums, red);
+  if (threadIdx.x != 0) return;
+  st->gamma = sums[0];
+  st->residual = sqrt(sums[1]) / st->bnorm;
+}
+
+// alpha = gamma / (p.v) with the breakdown rule of solvers.py:302-310
+static __global__ void k_std_alpha(const double* __restrict__ partials, int rows, SolveState* st) {
+  __shared__ double red[7 * 32];
+  __shared__ double sums[8];
+  if (!st->active) return;
+  reduce_rows(partials, rows, 1, sums, red);
+  if (threadIdx.x != 0) return;
+  const double a = sums[0];
+  if (a <= 0.0) {
+    if (st->fixed && st->residual < st->tol) st->alpha = 0.0;
+    else { st->breakdown = 1; st->breakdown_value = a; st->breakdown_iteration = st->k + 1; st->active = 0; }
+  } else {
+    st->alpha = st->gamma / a;
+  }
+}
+
+// y += sign * alpha * x
+template <typename T>
+__global__ void k_std_axpy(i64 n, T* __restrict__ y, const T* __restrict__ x, double sign, const SolveState* st) {
+  if (!st->active) return;
+  const T al = (T)(sign * st->alpha);
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    y[i] += al * x[i];
+}
+
+template <typename T>
+__global__ void k_std_prec(i64 n, T* __restrict__ Z, const T* __restrict__ Minv, const T* __restrict__ R,
+                           const SolveState* st) {
+  if (!st->active) return;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    Z[i] = Minv[i] * R[i];
+}
+
+// beta, residual, history (solvers.py:317-333); rr_partials: r.r, rz_partials: r.z (PCG only)
+static __global__ void k_std_beta(const double* __restrict__ rr_partials, const double* __restrict__ rz_partials,
+                           int rows, SolveState* st, double* __restrict__ history) {
+  __shared__ double red[7 * 32];
+  __shared__ double sums[8];
+  __shared__ double sums2[8];
+  if (!st->active) return;
+  reduce_rows(rr_partials, rows, 1, sums, red);
+  if (rz_partials) reduce_rows(rz_partials, rows, 1, sums2, red);
+  if (threadIdx.x != 0) return;
+  const double rr = sums[0];
+  const double gamma_new = rz_partials ? sums2[0] : rr;
+  const double residual = sqrt(rr) / st->bnorm;
+  const double beta = st->gamma > 0.0 ? gamma_new / st->gamma : 0.0;
+  const int k = st->k + 1;
+  history[(i64)(k - 1) * 4 + 0] = st->alpha;
+  history[(i64)(k - 1) * 4 + 1] = beta;
+  history[(i64)(k - 1) * 4 + 2] = st->gamma;
+  history[(i64)(k - 1) * 4 + 3] = residual;
+  st->gamma = gamma_new;
+  st->beta = beta;
+  st->residual = residual;
+  st->k = k;
+  if (!st->fixed && residual < st->tol) { st->converged = 1; st->active = 0; }
+  if (k >= st->limit) st->active = 0;
+}
+
+// p = beta p + z.  Runs even on the iteration that hit the limit in the
+// reference (solvers.py:334-335 executes unless the loop broke on convergence);
+// p is not observable afterwards, so skipping it when inactive is equivalent.
+template <typename T>
+__global__ void k_std_update_p(i64 n, T* __restrict__ Pv, const T* __restrict__ Z, const SolveState* st) {
+  if (!st->active) return;
+  const T be = (T)st->beta;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    Pv[i] = be * Pv[i] + Z[i];
+}
+
+// ---------------------------------------------------------------------------
+// Numbering helpers
+
+struct LatticeMap {
+  int p, cells[3], B[3], mb[3];
+  const i64* ent_start;
+};
+
+__device__ __forceinline__ void seg_of(int I, int p, int B, int ncell, int mbd, int& s, int& o, int& len) {
+  const int W = p * B;
+  int m = I / W, rem = I - m * W;
+  if (m == mbd) { m = mbd - 1; rem = W; }
+  int bc = ncell - m * B;
+  if (bc > B) bc = B;
+  const int L = p * bc;
+  if (rem == 0) { s = 2 * m; o = 0; len = 1; }
+  else if (rem == L) { s = 2 * m + 2; o = 0; len = 1; }
+  else { s = 2 * m + 1; o = rem - 1; len = L - 1; }
+}
+
+// lattice point (I,J,K) of the rank's mesh -> index in brick numbering
+__device__ __forceinline__ i64 lattice_to_dev(const BrickGrid& g, int I, int J, int K) {
+  int sx, ox, lx, sy, oy, ly, sz, oz, lz;
+  seg_of(I, g.p, g.B[0], g.cells[0], g.mb[0], sx, ox, lx);
+  seg_of(J, g.p, g.B[1], g.cells[1], g.mb[1], sy, oy, ly);
+  seg_of(K, g.p, g.B[2], g.cells[2], g.mb[2], sz, oz, lz);
+  (void)lz;
+  const i64 e = ((i64)sz * (2 * g.mb[1] + 1) + sy) * (2 * g.mb[0] + 1) + sx;
+  return g.ent_start[e] + ox + (i64)lx * (oy + (i64)ly * oz);
+}
+
+// perm[user] = device index, from the caller's 27 block starts per cell
+// (dofs.py:119-135 expansion rule) and the structured cell position.
+static __global__ void k_build_perm(BrickGrid g, const int* __restrict__ blocks, i64 n_cells, int* __restrict__ perm) {
+  const int p = g.p, n = p + 1, npc = n * n * n;
+  for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < n_cells * npc; t += (i64)gridDim.x * blockDim.x) {
+    const i64 cell = t / npc;
+    const int node = (int)(t - cell * npc);
+    const int i = node % n, j = (node / n) % n, k = node / (n * n);
+    const int sx = i == 0 ? 0 : (i == p ? 2 : 1), sy = j == 0 ? 0 : (j == p ? 2 : 1), sz = k == 0 ? 0 : (k == p ? 2 : 1);
+    const int cxo = sx == 1 ? i - 1 : 0, cyo = sy == 1 ? j - 1 : 0, czo = sz == 1 ? k - 1 : 0;
+    const int mxe = sx == 1 ? p - 1 : 1, mye = sy == 1 ? p - 1 : 1;
+    const i64 user = (i64)blocks[cell * 27 + sx + 3 * sy + 9 * sz] + cxo + mxe * (cyo + mye * czo);
+    const int cx = (int)(cell % g.cells[0]), cy = (int)((cell / g.cells[0]) % g.cells[1]),
+              cz = (int)(cell / ((i64)g.cells[0] * g.cells[1]));
+    perm[user] = (int)lattice_to_dev(g, cx * p + i, cy * p + j, cz * p + k);
+  }
+}
+
+// dev[perm[u]] = (T) usr[u]
+template <typename T>
+__global__ void k_to_device_order(i64 n, const int* __restrict__ perm, const double* __restrict__ usr, T* __restrict__ dev) {
+  for (i64 u = blockIdx.x * (i64)blockDim.x + threadIdx.x; u < n; u += (i64)gridDim.x * blockDim.x)
+    dev[perm[u]] = (T)usr[u];
+}
+
+// usr[u] = (double) dev[perm[u]]
+template <typename T>
+__global__ void k_to_user_order(i64 n, const int* __restrict__ perm, const T* __restrict__ dev, double* __restrict__ usr) {
+  for (i64 u = blockIdx.x * (i64)blockDim.x + threadIdx.x; u < n; u += (i64)gridDim.x * blockDim.x)
+    usr[u] = (double)dev[perm[u]];
+}
+
+static __global__ void k_mark_constrained(i64 k, const i64* __restrict__ constrained, const int* __restrict__ perm,
+                                   i64 n_int, unsigned char* __restrict__ mask, int* __restrict__ error) {
+  for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < k; t += (i64)gridDim.x * blockDim.x) {
+    const i64 d = perm[constrained[t]];
+    if (d < n_int) *error = 1;  // a constrained DoF strictly inside a brick: not a boundary constraint
+    else mask[d - n_int] = 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Jacobi diagonal, GL collocation, affine geometry (operator.py:380-418):
+// diag_loc[k,j,i] = gx w_k w_j dd_i + gy w_k w_i dd_j + gz w_j w_i dd_k,
+// dd_i = sum_q w_q D[q,i]^2, g_d = det J / h_d^2.
+struct DiagTables {
+  double w[9], dd[9], g[3];
+};
+
+static __global__ void k_diag_affine(BrickGrid g, DiagTables t, i64 n_cells, double* __restrict__ diag) {
+  const int p = g.p, n = p + 1, npc = n * n * n;
+  for (i64 q = blockIdx.x * (i64)blockDim.x + threadIdx.x; q < n_cells * npc; q += (i64)gridDim.x * blockDim.x) {
+    const i64 cell = q / npc;
+    const int node = (int)(q - cell * npc);
+    const int i = node % n, j = (node / n) % n, k = node / (n * n);
+    const int cx = (int)(cell % g.cells[0]), cy = (int)((cell / g.cells[0]) % g.cells[1]),
+              cz = (int)(cell / ((i64)g.cells[0] * g.cells[1]));
+    const double val = t.g[0] * t.w[k] * t.w[j] * t.dd[i] + t.g[1] * t.w[k] * t.w[i] * t.dd[j] +
+                       t.g[2] * t.w[j] * t.w[i] * t.dd[k];
+    atomicAdd(&diag[lattice_to_dev(g, cx * p + i, cy * p + j, cz * p + k)], val);
+  }
+}
+
+// diag -> 1/diag with constrained entries 1; flags non-positive / non-finite
+static __global__ void k_diag_invert(BrickGrid g, double* __restrict__ diag, int* __restrict__ error) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < g.n_dofs; i += (i64)gridDim.x * blockDim.x) {
+    double d = diag[i];
+    if (i >= g.n_int && g.mask[i - g.n_int]) d = 1.0;
+    if (!(d > 0.0) || isinf(d)) *error = 1;
+    diag[i] = 1.0 / d;
+  }
+}
+
+template <typename TO, typename TI>
+__global__ void k_convert(i64 n, const TI* __restrict__ in, TO* __restrict__ out) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    out[i] = (TO)in[i];
+}
+
+template <typename T>
+__global__ void k_fill(i64 n, T* __restrict__ out, T value) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    out[i] = value;
+}
+
+}  // namespace mfcg
