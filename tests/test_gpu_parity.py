@@ -1,0 +1,208 @@
+"""GPU parity: every call goes through the C ABI (libmfcg_b200.so) and is checked
+against the CPU oracle on the same seeded inputs and against the committed
+reference fixtures.  Tolerances: integer tables bit-exact; one apply / diagonal
+1e-12 relative; CG scalars 1e-10 while the reference's own re-ordering envelope
+allows it."""
+import numpy as np
+import pytest
+
+import mfcg_oracle as orc
+from _problems import (APPLY_CASES, gpu_operator, hist_array, host_tables, oracle_problem, rel,
+                       seeded_rhs)
+
+pytestmark = pytest.mark.gpu
+
+
+def _solvers():
+    from paper_2205_08909_b200 import solvers
+    return solvers
+
+
+@pytest.mark.parametrize("ci", range(len(APPLY_CASES)))
+def test_apply_diag_perm_vs_fixture(golden, ci):
+    cells, p, nq, numb, con = APPLY_CASES[ci]
+    g = golden["apply"]
+    m, h, plan = host_tables(cells, p, constrain=con, numbering=numb)
+    op = gpu_operator(m, h, plan, p, nq)
+    perm = op.device_permutation()
+    assert np.array_equal(np.sort(perm), np.arange(h.n_dofs)), "brick numbering is not a bijection"
+    u = g[f"c{ci}_u"]
+    Au = op.apply(u)
+    assert rel(Au, g[f"c{ci}_Au"]) < 1e-12
+    if con:
+        assert np.array_equal(Au[h.constrained_dofs], u[h.constrained_dofs])
+        assert rel(op.compute_diagonal().inverse_diagonal, g[f"c{ci}_invdiag"]) < 1e-12
+    out = np.empty_like(u)
+    assert op.apply(u, out=out) is out and np.array_equal(out, Au) or rel(out, Au) < 1e-14
+    with pytest.raises(ValueError):
+        op.apply(u[:-1])
+
+
+@pytest.mark.parametrize("brick", [(1, 1, 1), (2, 3, 2), (4, 4, 1), (3, 2, 5)])
+def test_apply_independent_of_brick_shape(brick):
+    cells, p, nq = (7, 5, 6), 5, 6
+    m, h, plan = host_tables(cells, p)
+    prob = oracle_problem(m, h, p, nq)
+    u = np.random.default_rng(5).standard_normal(h.n_dofs)
+    ref = orc.apply(prob, u)
+    op = gpu_operator(m, h, plan, p, nq, brick=brick)
+    assert op.info()["brick"] == brick
+    assert rel(op.apply(u), ref) < 1e-12
+    assert rel(op.compute_diagonal().inverse_diagonal, orc.inverse_diagonal(prob)) < 1e-12
+
+
+def test_linearity_symmetry_nullspace():
+    m, h, plan = host_tables((6, 5, 9), 5, constrain=False)
+    op = gpu_operator(m, h, plan, 5, 6)
+    rng = np.random.default_rng(11)
+    a, b = rng.standard_normal(h.n_dofs), rng.standard_normal(h.n_dofs)
+    Aa, Ab = op.apply(a), op.apply(b)
+    assert rel(op.apply(2.0 * a - 3.0 * b), 2.0 * Aa - 3.0 * Ab) < 1e-12
+    assert abs(a @ Ab - b @ Aa) < 1e-10 * abs(a @ Ab)
+    assert np.max(np.abs(op.apply(np.ones(h.n_dofs)))) < 1e-11
+
+
+def test_config1_solves_vs_reference(golden):
+    """BASELINE configs[0]: 8^3 cells Q4, 100 fixed iterations, all four variants."""
+    S = _solvers()
+    g = golden["config1"]
+    m, h, plan = host_tables((8, 8, 8), 4)
+    op = gpu_operator(m, h, plan, 4, 5)
+    b = g["b"]
+    assert np.array_equal(b, seeded_rhs(h))
+    assert rel(op.apply(b), g["Ab"]) < 1e-12
+    minv = op.compute_diagonal()
+    assert rel(minv.inverse_diagonal, g["invdiag"]) < 1e-12
+    cfg = S.SolverConfig(fixed_iterations=100)
+    for variant in ("pcg", "combined_pcg", "cg", "combined_cg"):
+        for fused in ((True, False) if variant.startswith("combined") else (True,)):
+            res = S.solve(variant, op, b, minv=minv, config=S.SolverConfig(fixed_iterations=100, fused=fused))
+            H, R = hist_array(res.history), g[f"{variant}_hist"]
+            assert res.iterations == 100 and res.matvecs == 100 and H.shape == R.shape
+            dev = np.abs(H[:, 3] - R[:, 3]) / R[:, 3]
+            if variant in ("pcg", "combined_pcg"):
+                E = g[f"{variant}_hist_reordered"]
+                env = np.maximum.accumulate(np.abs(E[:, 3] - R[:, 3]) / R[:, 3])
+                strict = env < 1e-11
+                assert dev[strict].max() < 1e-10, (variant, fused, dev[strict].max())
+                assert np.all(dev[~strict] <= 10 * env[~strict] + 1e-10), (variant, fused)
+            assert dev[:40].max() < 1e-10
+            for col in range(3):
+                assert rel(H[:40, col], R[:40, col]) < 1e-10, (variant, fused, col)
+            assert rel(res.x, g[f"{variant}_x"]) < 1e-7
+            # true residual of the returned iterate agrees with the recurred one
+            true_res = np.linalg.norm(b - op.apply(res.x)) / np.linalg.norm(b)
+            assert abs(true_res - res.residual) < 1e-9
+    # a preconditioner passed as a plain array gives the same history
+    res2 = S.solve("combined_pcg", op, b, minv=np.array(minv.inverse_diagonal), config=cfg)
+    res1 = S.solve("combined_pcg", op, b, minv=minv, config=cfg)
+    assert rel(hist_array(res2.history)[:40], hist_array(res1.history)[:40]) < 1e-10
+
+
+def test_tolerance_termination_and_edge_cases(golden):
+    S = _solvers()
+    g = golden["config1"]
+    m, h, plan = host_tables((8, 8, 8), 4)
+    op = gpu_operator(m, h, plan, 4, 5)
+    minv = op.compute_diagonal()
+    for variant in ("pcg", "combined_pcg"):
+        res = S.solve(variant, op, g["b"], minv=minv, config=S.SolverConfig(tolerance=1e-6, max_iterations=500))
+        assert [res.iterations, int(res.converged)] == list(g[f"{variant}_tol_iters"])
+        assert len(res.history) == res.iterations
+        assert rel(hist_array(res.history)[:, 3], g[f"{variant}_tol_hist"][:, 3]) < 1e-8
+    zero = S.solve("combined_pcg", op, np.zeros(h.n_dofs), minv=minv)
+    assert zero.iterations == 0 and zero.converged and not zero.history and np.all(zero.x == 0)
+    with pytest.raises(ValueError):
+        S.solve("pcg", op, g["b"])
+    with pytest.raises(ValueError):
+        S.solve("combined_pcg", op, g["b"][:-1], minv=minv)
+    with pytest.raises(ValueError):
+        S.solve("pcg", op, g["b"], minv=np.ones(5))
+    # merged vs standard alpha/beta over 10 iterations (reference tests/test_solvers.py:115-131)
+    a = hist_array(S.solve("pcg", op, g["b"], minv=minv, config=S.SolverConfig(fixed_iterations=10)).history)
+    c = hist_array(S.solve("combined_pcg", op, g["b"], minv=minv, config=S.SolverConfig(fixed_iterations=10)).history)
+    assert rel(a[:, 0], c[:, 0]) < 1e-8 and rel(a[:, 1], c[:, 1]) < 1e-8
+    # force_x_updates gives the same solution (tests/test_solvers.py:252-257)
+    x1 = S.solve("combined_pcg", op, g["b"], minv=minv, config=S.SolverConfig(fixed_iterations=31)).x
+    x2 = S.solve("combined_pcg", op, g["b"], minv=minv,
+                 config=S.SolverConfig(fixed_iterations=31, force_x_updates=True)).x
+    assert rel(x1, x2) < 1e-9
+    # breakdown: negative "preconditioner" (tests/test_solvers.py:185-227)
+    with pytest.raises(S.SolverBreakdown):
+        S.solve("combined_pcg", op, g["b"], minv=-np.ones(h.n_dofs))
+
+
+def test_q5_small_vs_reference(golden):
+    """BASELINE configs[1], rungs 4^3 and 6^3 (Q5, 200 iterations), default and optimized numbering."""
+    S = _solvers()
+    g = golden["q5_small"]
+    for n, numb in ((4, "default"), (6, "default"), (4, "optimized")):
+        tag = f"n{n}_{numb}"
+        m, h, plan = host_tables((n, n, n), 5, numbering=numb)
+        op = gpu_operator(m, h, plan, 5, 6)
+        b = g[f"{tag}_b"]
+        assert np.array_equal(b, seeded_rhs(h))
+        minv = op.compute_diagonal()
+        for variant in ("pcg", "combined_pcg"):
+            res = S.solve(variant, op, b, minv=minv, config=S.SolverConfig(fixed_iterations=200))
+            H, R = hist_array(res.history), g[f"{tag}_{variant}_hist"]
+            assert H.shape == R.shape
+            assert (np.abs(H[:40, 3] - R[:40, 3]) / R[:40, 3]).max() < 1e-10, (tag, variant)
+            assert rel(H[:40, :2], R[:40, :2]) < 1e-10
+
+
+def test_midsize_vs_oracle_and_roundtrip():
+    """16^3 cells Q5 (5.3e5 DoFs): apply vs oracle, solve to tolerance, true residual."""
+    S = _solvers()
+    m, h, plan = host_tables((16, 16, 16), 5, numbering="optimized")
+    prob = oracle_problem(m, h, 5, 6)
+    op = gpu_operator(m, h, plan, 5, 6)
+    u = np.random.default_rng(2).standard_normal(h.n_dofs)
+    assert rel(op.apply(u), orc.apply(prob, u)) < 1e-12
+    minv = op.compute_diagonal()
+    assert rel(minv.inverse_diagonal, orc.inverse_diagonal(prob)) < 1e-12
+    b = seeded_rhs(h)
+    res = S.solve("combined_pcg", op, b, minv=minv, config=S.SolverConfig(tolerance=1e-9, max_iterations=2000))
+    assert res.converged
+    assert np.linalg.norm(b - op.apply(res.x)) / np.linalg.norm(b) < 2e-9
+    ref = S.solve("pcg", op, b, minv=minv, config=S.SolverConfig(tolerance=1e-9, max_iterations=2000))
+    assert ref.converged and abs(ref.iterations - res.iterations) <= 2
+    assert rel(res.x, ref.x) < 1e-6
+
+
+def test_fp32_variant():
+    """fp32 vectors/operator (BASELINE configs[3]): 1e-4 relative against the fp64 oracle."""
+    S = _solvers()
+    m, h, plan = host_tables((6, 6, 6), 3)
+    prob = oracle_problem(m, h, 3, 4)
+    op = gpu_operator(m, h, plan, 3, 4, precision="fp32")
+    u = np.random.default_rng(4).standard_normal(h.n_dofs)
+    assert rel(op.apply(u), orc.apply(prob, u)) < 1e-5
+    minv = orc.inverse_diagonal(prob)
+    b = seeded_rhs(h)
+    x, k, r, conv, hist = orc.combined_pcg(lambda v: orc.apply(prob, v), b, minv, fixed_iterations=20)
+    res = S.solve("combined_pcg", op, b, minv=minv, config=S.SolverConfig(fixed_iterations=20))
+    assert rel(hist_array(res.history)[:, 3], hist_array(hist)[:, 3]) < 1e-4
+    assert rel(res.x, x) < 1e-4
+
+
+@pytest.mark.parametrize("p", range(1, 9))
+def test_all_degrees_apply_and_short_solve(p):
+    S = _solvers()
+    cells = {1: (19, 18, 5), 2: (11, 12, 4), 3: (7, 8, 3), 4: (6, 5, 3), 5: (5, 4, 3), 6: (4, 3, 3),
+             7: (3, 3, 3), 8: (3, 2, 3)}[p]
+    m, h, plan = host_tables(cells, p)
+    prob = oracle_problem(m, h, p, p + 1)
+    op = gpu_operator(m, h, plan, p, p + 1)
+    u = np.random.default_rng(p).standard_normal(h.n_dofs)
+    assert rel(op.apply(u), orc.apply(prob, u)) < 1e-12
+    minv_ref = orc.inverse_diagonal(prob)
+    minv = op.compute_diagonal()
+    assert rel(minv.inverse_diagonal, minv_ref) < 1e-12
+    b = seeded_rhs(h)
+    mv = lambda v: orc.apply(prob, v)
+    for variant, fn in (("pcg", orc.pcg), ("combined_pcg", orc.combined_pcg)):
+        x, k, r, conv, hist = fn(mv, b, minv_ref, fixed_iterations=15)
+        res = S.solve(variant, op, b, minv=minv, config=S.SolverConfig(fixed_iterations=15))
+        assert rel(hist_array(res.history), hist_array(hist)) < 1e-10, (p, variant)
+        assert rel(res.x, x) < 1e-10
