@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""Benchmark of the merged-CG hot path (BASELINE.json metric: CG DoF*iterations/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A "step" is one fixed-iteration merged Jacobi-PCG solve (`--iters`, default 200)
+of the Q5 Poisson problem on a Cartesian mesh (BASELINE.json configs[1], top rung
+116^3 cells ~ 1.96e8 DoFs at N=1; configs[4] weak scaling 80^3 cells per GPU for
+N>1).  Inputs are seeded synthetic data (uniform[-1,1] RHS, seed 0), stated in
+the JSON line.  `value` times K solves with b and x resident in HBM; `e2e` times
+the same K solves through the public API `solve("combined_pcg", op, b_host, ...)`
+with pinned host buffers (H2D of b and D2H of x inside the timed region).
+
+`--impl reference` times the CPU implementation of the same path (the oracle
+port of the pure-Python reference; `oracle/_ref` cannot exist because the
+reference has no compiled sources) on the host cores on a bounded sample.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+for _p in (ROOT, ROOT / "oracle"):
+    if str(_p) not in sys.path:
+        sys.path.insert(0, str(_p))
+
+import numpy as np  # noqa: E402
+
+METRIC = "merged Jacobi-PCG throughput (n_dofs x CG iterations / s)"
+UNIT = "DoF*it/s"
+BYTES_PER_DOF_IT = 64.0  # r,p,v read+write, Minv read, x every 2nd iteration, fp64
+
+
+def measured_peak():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        try:
+            return float(json.loads(f.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.index)], stdout=subprocess.PIPE, text=True)
+            self.thread = threading.Thread(target=self._pump, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [s.strip() for s in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def build_problem(cells, p):
+    from paper_2205_08909_b200 import dofs, mesh as pmesh
+    mesh = pmesh.build_cartesian_mesh(cells)
+    h = dofs.distribute_dofs(mesh, p, 1, constrain_boundary=True)
+    plan = dofs.make_batches(mesh, dofs.batch_size(p, 1, 8), "morton")
+    return mesh, h, plan
+
+
+def seeded_rhs(h, out=None):
+    b = np.random.default_rng(0).uniform(-1.0, 1.0, h.n_dofs)
+    b[h.constrained_dofs] = 0.0
+    if out is not None:
+        out[:] = b
+        return out
+    return b
+
+
+def cpu_port_throughput(cells, p, iters, threads=None):
+    """The oracle port timed on the host: merged Jacobi-PCG, fixed iterations."""
+    import mfcg_oracle as orc
+    mesh, h, plan = build_problem(cells, p)
+    b = seeded_rhs(h)
+    try:
+        import mfcg_oracle_c as oc
+        if oc.available():
+            t, cores = oc.time_combined_pcg(cells, p, p + 1, h.cell_index_blocks, h.constrained_dofs,
+                                            h.n_dofs, b, iters, threads)
+            return h.n_dofs * iters / t, cores, "C/OpenMP restatement (oracle/mfcg_oracle.c)"
+    except ImportError:
+        pass
+    prob = orc.Problem(tuple(cells), mesh.extents, 0.0, p, p + 1, h.cell_index_blocks,
+                       h.constrained_dofs, h.n_dofs)
+    minv = orc.inverse_diagonal(prob)
+    t0 = time.perf_counter()
+    orc.combined_pcg(lambda v: orc.apply(prob, v), b, minv, fixed_iterations=iters)
+    t = time.perf_counter() - t0
+    return h.n_dofs * iters / t, 1, "NumPy restatement (oracle/mfcg_oracle.py)"
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    n = args.ref_cells
+    cells = (n, n, n)
+    n_dofs = (n * args.degree + 1) ** 3
+    times = []
+    cores = 1
+    kind_note = ""
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        thr, cores, kind_note = cpu_port_throughput(cells, args.degree, args.ref_iters)
+        if s >= args.warmup:
+            times.append(n_dofs * args.ref_iters / thr)
+    total = sum(times)
+    value = n_dofs * args.ref_iters * len(times) / total
+    sample = (f"{n}^3 cells Q{args.degree} ({n_dofs} DoFs), {args.ref_iters} merged-PCG iterations per step "
+              f"of the same seeded problem; {kind_note}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (uniform[-1,1] RHS, seed 0)",
+        "config": workload_config(args, args.gpus),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line))
+
+
+def workload_cells(args, n_gpus):
+    if args.cells:
+        return tuple(args.cells)
+    if n_gpus == 1:
+        return (116, 116, 116)
+    return (80, 80, 80 * n_gpus)
+
+
+def workload_config(args, n_gpus):
+    cells = workload_cells(args, n_gpus)
+    n_dofs = int(np.prod([c * args.degree + 1 for c in cells]))
+    which = ("BASELINE configs[1] top rung" if n_gpus == 1 and not args.cells
+             else ("BASELINE configs[4] weak scaling, 80^3 cells per GPU in z-slabs" if not args.cells
+                   else "custom"))
+    return {"workload": f"Q{args.degree} Poisson, Cartesian {cells[0]}x{cells[1]}x{cells[2]} cells, "
+                        f"{n_dofs} DoFs, fp64, Jacobi, seeded uniform[-1,1] RHS, {args.iters} merged-CG "
+                        f"iterations per step ({which})",
+            "cells": list(cells), "degree": args.degree, "n_dofs": n_dofs, "iterations_per_step": args.iters,
+            "variant": args.variant, "l2": "inputs larger than L2 (each vector >> 126 MB); no flush needed",
+            "parallelism": "1 GPU" if n_gpus == 1 else f"z-slabs x{n_gpus}"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cells", type=int, nargs=3, default=None)
+    ap.add_argument("--degree", type=int, default=5)
+    ap.add_argument("--iters", type=int, default=200)
+    ap.add_argument("--variant", default="combined_pcg")
+    ap.add_argument("--precision", default="fp64")
+    ap.add_argument("--brick", type=int, nargs=3, default=(0, 0, 0))
+    ap.add_argument("--ref-cells", type=int, default=12)
+    ap.add_argument("--ref-iters", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a B200: the hot path has no CPU fallback")
+    if world > 1:
+        raise SystemExit("multi-GPU slabs: run through bench_slabs (not built in this revision)")
+    torch.cuda.set_device(local_rank)
+    from paper_2205_08909_b200 import _lib
+    from paper_2205_08909_b200.mesh import GeometryVariant
+    from paper_2205_08909_b200.operator import MatrixFreeOperator, OperatorSpec
+    from paper_2205_08909_b200.solvers import SolverConfig, solve, solve_device
+
+    p = args.degree
+    cells = workload_cells(args, 1)
+    t_setup = time.perf_counter()
+    mesh, h, plan = build_problem(cells, p)
+    op = MatrixFreeOperator(OperatorSpec("laplace", 1, p, p + 1, GeometryVariant.AFFINE), mesh, h, plan,
+                            device=local_rank, precision=args.precision, brick=tuple(args.brick))
+    info = op.info()
+    n = h.n_dofs
+    minv = op.compute_diagonal()
+    b_host = torch.empty(n, dtype=torch.float64).pin_memory()
+    x_host = torch.empty(n, dtype=torch.float64).pin_memory()
+    seeded_rhs(h, b_host.numpy())
+    b_dev = b_host.cuda()
+    x_dev = torch.empty_like(b_dev)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t_setup
+    cfg = SolverConfig(fixed_iterations=args.iters)
+    lib_stream = torch.cuda.ExternalStream(_lib.stream_handle(local_rank))
+
+    def step_dev(timed=False):
+        return solve_device(args.variant, op, b_dev.data_ptr(), x_dev.data_ptr(), minv=minv, config=cfg,
+                            time_kernels=timed)
+
+    for _ in range(args.warmup):
+        step_dev()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    launches = 0
+    e0.record(lib_stream)
+    for _ in range(args.steps):
+        res = step_dev()
+        launches += res.device_stats["kernel_launches"]
+    e1.record(lib_stream)
+    torch.cuda.synchronize()
+    ms_total = e0.elapsed_time(e1)
+    clocks = sampler.stop()
+    value = n * args.iters * args.steps / (ms_total * 1e-3)
+    residual = res.residual
+
+    # dominant kernel, timed per launch with CUDA events on the library stream
+    rt = step_dev(timed=True)
+    op_ms = rt.device_stats["operator_ms"] / max(rt.device_stats["operator_launches"], 1)
+    n_int, n_sh = info["n_interior"], n - info["n_interior"]
+    w = 8 if args.precision == "fp64" else 4
+    kernel_bytes = 8 * w * n_int + 2 * w * n_sh  # interior: the full 8 scalars; shared: read p, add to v
+    peak, peak_src = measured_peak()
+    achieved = kernel_bytes / (op_ms * 1e-3) / 1e9
+    it_ms = rt.device_stats["solve_ms"] / args.iters
+    roofline = {
+        "bound": "hbm", "kernel": f"k_brick<{p},{'double' if w == 8 else 'float'},merged>",
+        "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
+        "traffic": None, "algorithmic_bytes_per_launch": kernel_bytes, "kernel_ms": op_ms,
+        "iteration_ms": it_ms, "kernel_share_of_step": op_ms / it_ms,
+        "iteration_frac": (8 * w * n) / (it_ms * 1e-3) / 1e9 / peak,
+        "whole_solve_frac": value * 8 * w / 1e9 / peak,
+    }
+    prof = ROOT / "profiles" / "traffic.json"
+    if prof.exists():
+        try:
+            roofline["traffic"] = json.loads(prof.read_text()).get("k_brick_merged_bytes_per_launch")
+        except Exception:
+            pass
+
+    # end to end through the public API: pinned host b in, pinned host x out, every step
+    for _ in range(1):
+        solve(args.variant, op, b_host.numpy(), minv=minv, config=cfg, out=x_host.numpy())
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2e_launches = 0
+    for _ in range(args.steps):
+        r2 = solve(args.variant, op, b_host.numpy(), minv=minv, config=cfg, out=x_host.numpy())
+        e2e_launches += r2.device_stats["kernel_launches"]
+    torch.cuda.synchronize()
+    t_e2e = time.perf_counter() - t0
+    e2e = {"value": n * args.iters * args.steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
+           "d2h_bytes_per_step": 8 * n + 32 * args.iters, "ms_per_step": 1e3 * t_e2e / args.steps,
+           "timer": "host wall clock around K public-API solves, synchronised both sides"}
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        nref = args.ref_cells
+        thr, cores, note = cpu_port_throughput((nref, nref, nref), p, args.ref_iters)
+        cpu = {"value": thr, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{nref}^3 cells Q{p} ({(nref * p + 1) ** 3} DoFs), {args.ref_iters} merged-PCG "
+                         f"iterations; {note}"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64" if w == 8 else "f32",
+        "data": "synthetic (uniform[-1,1] RHS, seed 0, constrained entries zeroed)",
+        "config": workload_config(args, 1), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": int(launches), "clocks": clocks,
+        "extra": {"final_relative_residual": residual, "bricks": info["n_bricks"], "brick": info["brick"],
+                  "interior_fraction": n_int / n, "setup_seconds": t_setup,
+                  "timer": "CUDA events on the library stream around K device-resident solves"},
+    }
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

@@ -62,6 +62,8 @@ typedef struct mfcg_op mfcg_op;
 int mfcg_ctx_create(int device, mfcg_ctx** ctx);
 void mfcg_ctx_destroy(mfcg_ctx* ctx);
 const char* mfcg_last_error(void);
+/* The cudaStream_t all work of this context is enqueued on (for event timing by the caller). */
+void* mfcg_ctx_stream(mfcg_ctx* ctx);
 
 /*
  * Operator description == arguments of `MatrixFreeOperator(spec, mesh, handler,

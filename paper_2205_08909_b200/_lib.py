@@ -68,7 +68,7 @@ class SolveResultC(C.Structure):
 
 
 EXPORTS = (
-    "mfcg_ctx_create", "mfcg_ctx_destroy", "mfcg_last_error", "mfcg_op_create",
+    "mfcg_ctx_create", "mfcg_ctx_destroy", "mfcg_ctx_stream", "mfcg_last_error", "mfcg_op_create",
     "mfcg_op_destroy", "mfcg_op_get_info", "mfcg_op_device_permutation",
     "mfcg_op_apply", "mfcg_op_diagonal", "mfcg_op_geometry", "mfcg_solve",
     "mfcg_comm_unique_id", "mfcg_ctx_init_comm",
@@ -91,6 +91,8 @@ def load():
     lib.mfcg_last_error.restype = C.c_char_p
     lib.mfcg_ctx_create.argtypes = [C.c_int, C.POINTER(vp)]
     lib.mfcg_ctx_destroy.argtypes = [vp]
+    lib.mfcg_ctx_stream.argtypes = [vp]
+    lib.mfcg_ctx_stream.restype = vp
     lib.mfcg_ctx_destroy.restype = None
     lib.mfcg_op_create.argtypes = [vp, C.POINTER(OpDesc), C.POINTER(vp)]
     lib.mfcg_op_destroy.argtypes = [vp]
@@ -143,3 +145,8 @@ def context(device: int = 0):
         check(lib.mfcg_ctx_create(device, C.byref(ctx)))
         _contexts[device] = ctx
     return _contexts[device]
+
+
+def stream_handle(device: int = 0) -> int:
+    """Raw cudaStream_t of the library context (wrap with torch.cuda.ExternalStream)."""
+    return int(load().mfcg_ctx_stream(context(device)))

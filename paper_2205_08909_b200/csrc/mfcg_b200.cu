@@ -81,6 +81,8 @@ int mfcg_ctx_create(int device, mfcg_ctx** out) {
   return MFCG_OK;
 }
 
+void* mfcg_ctx_stream(mfcg_ctx* ctx) { return ctx ? (void*)ctx->c.stream : nullptr; }
+
 void mfcg_ctx_destroy(mfcg_ctx* ctx) {
   if (!ctx) return;
   if (ctx->c.stream) cudaStreamDestroy(ctx->c.stream);

@@ -75,7 +75,7 @@ _BREAKDOWN_TEXT = {
 
 
 def _run(variant: str, A, b, minv, cfg: SolverConfig, recorder, *, location=0, x_out=None,
-         time_kernels=False):
+         time_kernels=False, out=None):
     if recorder is not None:
         raise NotImplementedError("access recorders are not supported on the GPU solvers")
     if not isinstance(A, MatrixFreeOperator):
@@ -90,7 +90,12 @@ def _run(variant: str, A, b, minv, cfg: SolverConfig, recorder, *, location=0, x
         bb = np.ascontiguousarray(b, dtype=np.float64)
         keep.append(bb)
         args.b = bb.ctypes.data
-        x = np.empty(n)
+        if out is not None:
+            if out.dtype != np.float64 or not out.flags.c_contiguous or len(out) != n:
+                raise ValueError("out must be a contiguous float64 array of length n_dofs")
+            x = out
+        else:
+            x = np.empty(n)
         args.x = x.ctypes.data
     else:
         args.b = int(b)
@@ -166,8 +171,18 @@ def solve_combined_pcg(A, b, minv, config: SolverConfig = None, *, recorder=None
     return _run("combined_pcg", A, b, minv, config or SolverConfig(), recorder)
 
 
-def solve(variant: str, A, b, *, minv=None, config: SolverConfig = None, recorder=None) -> SolveResult:
-    """Dispatch by variant name (solvers.py:816-834)."""
+def solve(variant: str, A, b, *, minv=None, config: SolverConfig = None, recorder=None,
+          out: np.ndarray = None, time_kernels: bool = False) -> SolveResult:
+    """Dispatch by variant name (solvers.py:816-834).  Extensions: `out` receives
+    the solution (e.g. a pinned buffer) instead of a fresh array; `time_kernels`
+    adds per-launch CUDA-event timing of the operator kernel to the result."""
+    if out is not None or time_kernels:
+        if variant not in VARIANTS:
+            raise ValueError(f"unknown solver variant {variant!r}")
+        if variant in ("pcg", "combined_pcg") and minv is None:
+            raise ValueError(f"{variant} requires a preconditioner")
+        return _run(variant, A, b, minv, config or SolverConfig(), recorder, out=out,
+                    time_kernels=time_kernels)
     if variant == "cg":
         return solve_cg(A, b, config, recorder=recorder)
     if variant == "pcg":
