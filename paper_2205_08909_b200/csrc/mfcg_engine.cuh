@@ -76,7 +76,8 @@ class Engine : public EngineBase {
 
   int init() {
     const double det = c_->h[0] * c_->h[1] * c_->h[2];
-    // M = S^T W S, K = D^T W D on [0,1] (tensor.py tables), scaled per direction
+    // M = S^T W S, K = D^T W D on [0,1] (tensor.py tables), split into packed even/odd halves
+    std::vector<double> M(N * N), K(N * N);
     for (int i = 0; i < N; ++i)
       for (int j = 0; j < N; ++j) {
         double m = 0.0, k = 0.0;
@@ -84,11 +85,33 @@ class Engine : public EngineBase {
           m += c_->wq[q] * c_->S[q * N + i] * c_->S[q * N + j];
           k += c_->wq[q] * c_->D[q * N + i] * c_->D[q * N + j];
         }
-        tab_.M[i * N + j] = (T)m;
-        tab_.Kx[i * N + j] = (T)(k * det / (c_->h[0] * c_->h[0]));
-        tab_.Ky[i * N + j] = (T)(k * det / (c_->h[1] * c_->h[1]));
-        tab_.Kz[i * N + j] = (T)(k * det / (c_->h[2] * c_->h[2]));
+        M[i * N + j] = m;
+        K[i * N + j] = k;
       }
+    // enforce the exact symmetries the packed storage assumes (they hold to rounding)
+    auto symmetrise = [&](std::vector<double>& A) {
+      for (int i = 0; i < N; ++i)
+        for (int j = 0; j < N; ++j) {
+          const double v = 0.25 * (A[i * N + j] + A[j * N + i] + A[(N - 1 - i) * N + (N - 1 - j)] +
+                                   A[(N - 1 - j) * N + (N - 1 - i)]);
+          A[i * N + j] = A[j * N + i] = A[(N - 1 - i) * N + (N - 1 - j)] = A[(N - 1 - j) * N + (N - 1 - i)] = v;
+        }
+    };
+    symmetrise(M);
+    symmetrise(K);
+    constexpr int H = EOShape<N>::H, HE = EOShape<N>::HE;
+    auto pack = [&](const std::vector<double>& A, T* Ae, T* Ao) {
+      for (int i = 0; i < HE; ++i)
+        for (int j = i; j < HE; ++j) {
+          const bool mid = (N & 1) && (j == H);
+          Ae[sym_idx(i, j)] = (T)(mid ? A[i * N + j] : 0.5 * (A[i * N + j] + A[i * N + (N - 1 - j)]));
+        }
+      for (int i = 0; i < H; ++i)
+        for (int j = i; j < H; ++j) Ao[sym_idx(i, j)] = (T)(0.5 * (A[i * N + j] - A[i * N + (N - 1 - j)]));
+    };
+    pack(M, tab_.Me, tab_.Mo);
+    pack(K, tab_.Ke, tab_.Ko);
+    for (int d = 0; d < 3; ++d) tab_.g[d] = (T)(det / (c_->h[d] * c_->h[d]));
     // the mass factor of the cell volume is carried by the K's: A_e = sum_d Kd (x) M (x) M
     smem_ = (int)Geo<P>::template smem_bytes<T>();
     MFCG_CUDA(cudaFuncSetAttribute(k_brick<P, T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
@@ -235,12 +258,20 @@ class Engine : public EngineBase {
 
   // dst = A src in brick numbering
   int launch_apply(const T* src, T* dst) {
-    if (c_->grid.n_dofs > c_->grid.n_int) {
-      k_surface_init<T><<<vgrid_, VT, 0, stream()>>>(c_->grid, src, dst);
+    const bool has_shared = c_->grid.n_dofs > c_->grid.n_int;
+    if (has_shared) {
+      k_surface_init<T><<<vgrid_, VT, 0, stream()>>>(c_->grid, dst);
       MFCG_CUDA(cudaGetLastError());
       ++launches_;
     }
-    return launch_brick(0, src, nullptr, dst, nullptr);
+    int rc = launch_brick(0, src, nullptr, dst, nullptr);
+    if (rc) return rc;
+    if (has_shared) {
+      k_surface_fix<T><<<vgrid_, VT, 0, stream()>>>(c_->grid, src, dst);
+      MFCG_CUDA(cudaGetLastError());
+      ++launches_;
+    }
+    return MFCG_OK;
   }
 
   int run_merged(const mfcg_solve_args* a, int limit);
@@ -273,7 +304,7 @@ int Engine<P, T>::run_merged(const mfcg_solve_args* a, int limit) {
       int rc = launch_brick(1, nullptr, p_, v_, partials_a_);
       if (rc) return rc;
       if (n_sh > 0) {
-        k_post<T><<<vgrid_, VT, 0, stream()>>>(g.n_int, n, r_, p_, v_, minv_, c_->d_state,
+        k_post<T><<<vgrid_, VT, 0, stream()>>>(g, g.n_int, n, 1, r_, p_, v_, minv_, c_->d_state,
                                                partials_a_ + 8 * c_->n_bricks);
         ++launches_;
       }
@@ -284,7 +315,7 @@ int Engine<P, T>::run_merged(const mfcg_solve_args* a, int limit) {
       k_pre<T><<<vgrid_, VT, 0, stream()>>>(g, 0, n, 0, r_, p_, v_, x_, minv_, c_->d_state);
       int rc = launch_apply(p_, v_);
       if (rc) return rc;
-      k_post<T><<<vgrid_, VT, 0, stream()>>>(0, n, r_, p_, v_, minv_, c_->d_state, partials_a_);
+      k_post<T><<<vgrid_, VT, 0, stream()>>>(g, 0, n, 0, r_, p_, v_, minv_, c_->d_state, partials_a_);
       k_scalar_merged<<<1, 256, 0, stream()>>>(partials_a_, vgrid_, c_->d_state, d_history_);
       launches_ += 3;
     }

@@ -50,17 +50,24 @@ struct SolveState {
   double gamma, alpha, beta;  // standard (P)CG scalars
 };
 
+// Per-degree launch shape of the brick kernel: BX x BY cells per brick layer,
+// NT_C "math" threads (sum-factorisation sweeps, shared memory only), NT_P
+// "memory" threads (all global loads: pre on the way in, post one layer behind),
+// KC lattice planes per load batch (memory-level parallelism per thread).
 template <int P> struct Cfg;
-#define MFCG_CFG(P_, B_, T_, MB_) \
-  template <> struct Cfg<P_> { static constexpr int BX = B_, BY = B_, THREADS = T_, MINB = MB_; };
-MFCG_CFG(1, 16, 512, 2)
-MFCG_CFG(2, 10, 320, 2)
-MFCG_CFG(3, 6, 288, 2)
-MFCG_CFG(4, 5, 320, 2)
-MFCG_CFG(5, 4, 288, 2)
-MFCG_CFG(6, 3, 224, 2)
-MFCG_CFG(7, 2, 256, 2)
-MFCG_CFG(8, 2, 192, 2)
+#define MFCG_CFG(P_, B_, TC_, TP_, KC_, MB_)                                                   \
+  template <> struct Cfg<P_> {                                                                 \
+    static constexpr int BX = B_, BY = B_, NT_C = TC_, NT_P = TP_, KC = KC_, MINB = MB_,       \
+                         THREADS = TC_ + TP_;                                                  \
+  };
+MFCG_CFG(1, 16, 256, 128, 2, 2)
+MFCG_CFG(2, 10, 256, 128, 3, 2)
+MFCG_CFG(3, 6, 192, 128, 4, 2)
+MFCG_CFG(4, 5, 224, 128, 3, 2)
+MFCG_CFG(5, 4, 192, 128, 3, 2)
+MFCG_CFG(6, 3, 224, 128, 3, 2)
+MFCG_CFG(7, 2, 128, 128, 4, 2)
+MFCG_CFG(8, 2, 128, 128, 3, 2)
 
 template <int P> struct Geo {
   static constexpr int N = P + 1;
@@ -69,20 +76,62 @@ template <int P> struct Geo {
   static constexpr int NCELL = Cfg<P>::BX * Cfg<P>::BY;
   static constexpr int WX = P * Cfg<P>::BX + 1;         // window row stride (odd for every Cfg)
   static constexpr int PLANE = WX * (P * Cfg<P>::BY + 1);
+  static constexpr int RB = 2 * P + 1;                  // lattice planes in the ring: two layers share one
   template <typename T> __host__ __device__ static constexpr size_t red_offset() {
-    return (256 + sizeof(T) * (size_t)(N * PLANE + PLANE + 2 * NCELL * TILE) + 15) & ~(size_t)15;
+    return (256 + sizeof(T) * (size_t)(RB * PLANE + PLANE + 2 * NCELL * TILE) + 15) & ~(size_t)15;
   }
   template <typename T> __host__ __device__ static constexpr size_t smem_bytes() { return red_offset<T>() + 8 * 7 * 32; }
 };
 
 // 1D matrices of the separable (Cartesian/affine) cell operator
-//   A_e = Kx (x) M (x) M + M (x) Ky (x) M + M (x) M (x) Kz,
-// M = S^T W S, Kd = (det J / h_d^2) D^T W D, rows = output index.  Passed by
-// value: kernel parameters sit in the constant bank, so every entry is an
-// immediate c[0x0][..] operand of the DFMA.
-template <typename T, int N> struct SepTables {
-  T M[N * N], Kx[N * N], Ky[N * N], Kz[N * N];
+//   A_e = gx K (x) M (x) M + gy M (x) K (x) M + gz M (x) M (x) K,
+// M = S^T W S, K = D^T W D on [0,1], g_d = det J / h_d^2.  Both matrices are
+// symmetric and centro-symmetric, so a product with a line u splits into an
+// even part (acting on u_j + u_{N-1-j}) and an odd part (on u_j - u_{N-1-j}),
+// each a symmetric half-size matrix (the even-odd decomposition the reference
+// uses in tensor.py:167-239, here additionally packed by symmetry).  For N = 6
+// that is 24 distinct doubles: they fit the uniform register file, so every
+// DFMA takes its coefficient as a UR operand with no shared-memory traffic.
+// Passed by value (kernel parameters live in the constant bank).
+template <int N> struct EOShape {
+  static constexpr int H = N / 2, HE = (N + 1) / 2;
+  static constexpr int NE = HE * (HE + 1) / 2, NO = H * (H + 1) / 2 > 0 ? H * (H + 1) / 2 : 1;
 };
+template <typename T, int N> struct SepTables {
+  T Me[EOShape<N>::NE], Mo[EOShape<N>::NO], Ke[EOShape<N>::NE], Ko[EOShape<N>::NO];
+  T g[3];
+};
+__host__ __device__ constexpr int sym_idx(int i, int j) { return i <= j ? j * (j + 1) / 2 + i : i * (i + 1) / 2 + j; }
+
+// e_j = u_j + u_{N-1-j}, o_j = u_j - u_{N-1-j}; the middle entry (odd N) goes to e
+template <int N, typename T>
+__device__ __forceinline__ void eo_split(const T* u, T* e, T* o) {
+  constexpr int H = EOShape<N>::H;
+#pragma unroll
+  for (int j = 0; j < H; ++j) { e[j] = u[j] + u[N - 1 - j]; o[j] = u[j] - u[N - 1 - j]; }
+  if (N & 1) e[H] = u[H];
+}
+// se += Ae e, so += Ao o with packed symmetric halves
+template <int N, typename T>
+__device__ __forceinline__ void eo_mul(const T* Ae, const T* Ao, const T* e, const T* o, T* se, T* so) {
+  constexpr int H = EOShape<N>::H, HE = EOShape<N>::HE;
+#pragma unroll
+  for (int i = 0; i < HE; ++i)
+#pragma unroll
+    for (int j = 0; j < HE; ++j) se[i] += Ae[sym_idx(i, j)] * e[j];
+#pragma unroll
+  for (int i = 0; i < H; ++i)
+#pragma unroll
+    for (int j = 0; j < H; ++j) so[i] += Ao[sym_idx(i, j)] * o[j];
+}
+// out_i = se_i + so_i, out_{N-1-i} = se_i - so_i
+template <int N, typename T>
+__device__ __forceinline__ void eo_join(const T* se, const T* so, T* out) {
+  constexpr int H = EOShape<N>::H;
+#pragma unroll
+  for (int i = 0; i < H; ++i) { out[i] = se[i] + so[i]; out[N - 1 - i] = se[i] - so[i]; }
+  if (N & 1) out[H] = se[H];
+}
 
 __device__ __forceinline__ int brick_cells(const BrickGrid& g, int d, int m) {
   int r = g.cells[d] - m * g.B[d];
@@ -113,21 +162,56 @@ __device__ __forceinline__ void block_reduce7_store(double* s, double* red, doub
 }
 
 // ---------------------------------------------------------------------------
+// mbarrier / named-barrier helpers (shared::cta)
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (!ok) __nanosleep(40);
+  } while (!ok);
+}
+template <int COUNT> __device__ __forceinline__ void math_barrier() {
+  asm volatile("bar.sync 1, %0;" ::"n"(COUNT) : "memory");
+}
+
+// ---------------------------------------------------------------------------
 // The brick kernel.  MODE 0: dst = A src (operator.py:285-360).
-// MODE 1: one merged-CG iteration on brick-interior DoFs (solvers.py:660-704):
-// pre on load, cell work, post on the finished values; shared DoFs have been
-// pre-updated by k_pre and receive atomic contributions.
+// MODE 1: one merged-CG iteration on brick-interior DoFs (solvers.py:660-704).
+//
+// One block = one brick, marched layer by layer in z.  Warp-specialised:
+//   memory warps  stream the next layer's lattice planes from HBM (MODE 1: r, v,
+//                 p, 1/diag, x of every interior DoF -> pre update -> r, p, x
+//                 written back, p into the shared-memory plane ring) while the
+//                 math warps work on the current layer, and run the seven post
+//                 sums one layer behind on values still resident in L2;
+//   math warps    never load from global memory: x/y/z even-odd sweeps in shared
+//                 memory, a deterministic gather of the cells' contributions per
+//                 lattice point, v stored (interior) or atomically added (shared).
+// Hand-over through two mbarrier pairs (full/empty per layer parity).
 template <int P, typename T, int MODE>
 __global__ void __launch_bounds__(Cfg<P>::THREADS, Cfg<P>::MINB)
 k_brick(BrickGrid g, SepTables<T, P + 1> tab, const T* __restrict__ src, T* __restrict__ Pv,
         T* __restrict__ V, T* __restrict__ R, T* __restrict__ X, const T* __restrict__ Minv,
         const SolveState* __restrict__ st, double* __restrict__ partials) {
   constexpr int N = P + 1, RS = Geo<P>::RS, TILE = Geo<P>::TILE, WX = Geo<P>::WX,
-                PLANE = Geo<P>::PLANE, NCELL = Geo<P>::NCELL, NT = Cfg<P>::THREADS;
+                PLANE = Geo<P>::PLANE, NCELL = Geo<P>::NCELL, RB = Geo<P>::RB,
+                NT_C = Cfg<P>::NT_C, NT_P = Cfg<P>::NT_P, KC = Cfg<P>::KC, HE = EOShape<N>::HE;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  i64* st27 = reinterpret_cast<i64*>(smem_raw);
-  T* Pw = reinterpret_cast<T*>(smem_raw + 256);
-  T* carry = Pw + N * PLANE;
+  i64* st27 = reinterpret_cast<i64*>(smem_raw);                               // 27 entity starts
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem_raw + 224);  // full[2], empty[2]
+  T* ring = reinterpret_cast<T*>(smem_raw + 256);
+  T* carry = ring + RB * PLANE;
   T* A = carry + PLANE;
   T* Bs = A + NCELL * TILE;
   constexpr size_t RED_OFF = Geo<P>::template red_offset<T>();
@@ -151,208 +235,288 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, const T* __restrict__ src, T* __re
     const int ex = tid % 3, ey = (tid / 3) % 3, ez = tid / 9;
     st27[tid] = g.ent_start[((i64)(2 * mz + ez) * (2 * g.mb[1] + 1) + (2 * my + ey)) * (2 * g.mb[0] + 1) + 2 * mx + ex];
   }
-  for (int i = tid; i < PLANE; i += NT) carry[i] = (T)0;
+  if (tid == 32) {
+    mbar_init(&bars[0], NT_P);
+    mbar_init(&bars[1], NT_P);
+    mbar_init(&bars[2], NT_C);
+    mbar_init(&bars[3], NT_C);
+  }
+  for (int i = tid; i < PLANE; i += NT_C + NT_P) carry[i] = (T)0;
   __syncthreads();
 
   const int fw = Lx + 1, fp = fw * (Ly + 1);
   const unsigned fw_magic = (65536u + fw - 1) / fw;
-  const int ncell = bcx * bcy;
-  const unsigned bcx_magic = (65536u + bcx - 1) / bcx;
   const i64 n_int = g.n_int;
   double s[7] = {0, 0, 0, 0, 0, 0, 0};
 
-  for (int kz = 0; kz < bcz; ++kz) {
-    const int k0 = kz == 0 ? 0 : 1;
-    // ---- load the layer's lattice planes (pre fused for interior DoFs)
-    for (int rem = tid; rem < fp; rem += NT) {
-      const int j = (int)(((unsigned)rem * fw_magic) >> 16);
-      const int i = rem - j * fw;
-      const int ex = i == 0 ? 0 : (i == Lx ? 2 : 1), ey = j == 0 ? 0 : (j == Ly ? 2 : 1);
-      const int ox = ex == 1 ? i - 1 : 0, oy = ey == 1 ? j - 1 : 0;
-      const int lx = ex == 1 ? Lx - 1 : 1, ly = ey == 1 ? Ly - 1 : 1;
-      const bool edge = (ex != 1) || (ey != 1);
+  if (tid >= NT_C) {
+    // ===================== memory warps =====================
+    const int ptid = tid - NT_C;
+    for (int L = 0; L < bcz + 2; ++L) {
+      const int stage = L & 1;
+      if (L >= 2) mbar_wait(&bars[2 + stage], ((L >> 1) - 1) & 1);  // layer L-2 consumed
+      if (L < bcz) {
+        // ---- fill the ring with the planes layer L adds (plane 0 is shared with layer L-1)
+        const int k0 = L == 0 ? 0 : 1;
+        const int s0 = (L * P) % RB;
+        for (int rem = ptid; rem < fp; rem += NT_P) {
+          const int j = (int)(((unsigned)rem * fw_magic) >> 16);
+          const int i = rem - j * fw;
+          const int ex = i == 0 ? 0 : (i == Lx ? 2 : 1), ey = j == 0 ? 0 : (j == Ly ? 2 : 1);
+          const int ox = ex == 1 ? i - 1 : 0, oy = ey == 1 ? j - 1 : 0;
+          const int lx = ex == 1 ? Lx - 1 : 1, ly = ey == 1 ? Ly - 1 : 1;
+          const bool edge = (ex != 1) || (ey != 1);
+          const int e2 = ex + 3 * ey, o2 = ox + lx * oy, pstride = lx * ly;
+          T* rp = ring + j * WX + i;
 #pragma unroll
-      for (int k = 0; k <= P; ++k) {
-        if (k < k0) continue;
-        const int K = kz * P + k;
-        const int ez = K == 0 ? 0 : (K == Lz ? 2 : 1);
-        const int oz = ez == 1 ? K - 1 : 0;
-        const i64 gi = st27[ex + 3 * ey + 9 * ez] + ox + (i64)lx * (oy + ly * oz);
-        const bool shared = edge || ez != 1;
-        T val;
-        if (MODE == 0) {
-          val = src[gi];
-          if (shared && g.mask[gi - n_int]) val = (T)0;
-        } else {
-          if (!shared) {
-            T r = R[gi], v = V[gi], p = Pv[gi];
-            const T m = Minv[gi];
-            if (xmode) {
-              T x = X[gi];
-              if (xmode == 2) x += xc1 * p + xc2 * (p - m * r);
-              else x += xc1 * p;
-              X[gi] = x;
+          for (int kb = 0; kb <= P; kb += KC) {
+            i64 gi[KC];
+            bool sh[KC], on[KC];
+            unsigned char mk[KC];
+            T rr[KC], vv[KC], pp[KC], mm[KC], xx[KC];
+            // issue every load of the batch before any value is used: no load may
+            // depend on loaded data, or the warp pays one DRAM round trip per plane
+#pragma unroll
+            for (int c = 0; c < KC; ++c) {
+              const int k = kb + c;
+              on[c] = k <= P && k >= k0;
+              const int K = L * P + k;
+              const int ez = K == 0 ? 0 : (K == Lz ? 2 : 1);
+              gi[c] = st27[e2 + 9 * ez] + o2 + (ez == 1 ? (i64)pstride * (K - 1) : 0);
+              sh[c] = edge || ez != 1;
+              rr[c] = vv[c] = mm[c] = xx[c] = pp[c] = (T)0;
+              mk[c] = 0;
+              if (on[c]) {
+                pp[c] = MODE == 0 ? src[gi[c]] : Pv[gi[c]];
+                if (sh[c]) {
+                  mk[c] = g.mask[gi[c] - n_int];
+                } else if (MODE == 1) {
+                  rr[c] = R[gi[c]]; vv[c] = V[gi[c]]; mm[c] = Minv[gi[c]];
+                  if (xmode) xx[c] = X[gi[c]];
+                }
+              }
             }
-            r -= am1 * v;
-            p = m * r + bm1 * p;
-            R[gi] = r;
-            Pv[gi] = p;
-            val = p;
-          } else {
-            val = g.mask[gi - n_int] ? (T)0 : Pv[gi];
+#pragma unroll
+            for (int c = 0; c < KC; ++c) {
+              const int k = kb + c;
+              if (!on[c]) continue;
+              T val = mk[c] ? (T)0 : pp[c];
+              if (MODE == 1 && !sh[c]) {
+                T r = rr[c], p = pp[c];
+                if (xmode) {
+                  T x = xx[c];
+                  if (xmode == 2) x += xc1 * p + xc2 * (p - mm[c] * r);
+                  else x += xc1 * p;
+                  X[gi[c]] = x;
+                }
+                r -= am1 * vv[c];
+                p = mm[c] * r + bm1 * p;
+                R[gi[c]] = r;
+                Pv[gi[c]] = p;
+                val = p;
+              }
+              int slot = s0 + k;
+              if (slot >= RB) slot -= RB;
+              rp[slot * PLANE] = val;
+            }
           }
         }
-        Pw[k * PLANE + j * WX + i] = val;
+        mbar_arrive(&bars[stage]);  // layer L full
       }
-    }
-    __syncthreads();
-
-    // ---- x sweep: a = M u, b = Kx u along every x line of every cell
-    for (int w = tid; w < ncell * N * N; w += NT) {
-      const int cell = w / (N * N);
-      const int rr = w - cell * (N * N);
-      const int k = rr / N, j = rr - k * N;
-      const int cy = (int)(((unsigned)cell * bcx_magic) >> 16);
-      const int cx = cell - cy * bcx;
-      const T* row = Pw + k * PLANE + (cy * P + j) * WX + cx * P;
-      T u[N];
+      if (MODE == 1 && L >= 2) {
+        // ---- post sums of layer L-2 (its v is final and, like r, p, 1/diag, still in L2)
+        const int Lp = L - 2;
+        const int Klo = Lp == 0 ? 1 : Lp * P, Khi = Lp * P + P - 1;  // interior planes finished by layer Lp
+        for (int rem = ptid; rem < fp; rem += NT_P) {
+          const int j = (int)(((unsigned)rem * fw_magic) >> 16);
+          const int i = rem - j * fw;
+          if (i == 0 || i == Lx || j == 0 || j == Ly) continue;
+          const i64 base = st27[13] + (i - 1) + (i64)(Lx - 1) * (j - 1);
+          const i64 pstride = (i64)(Lx - 1) * (Ly - 1);
 #pragma unroll
-      for (int i = 0; i < N; ++i) u[i] = row[i];
-      T* ao = A + cell * TILE + (k * N + j) * RS;
-      T* bo = Bs + cell * TILE + (k * N + j) * RS;
-#pragma unroll
-      for (int q = 0; q < N; ++q) {
-        T a = 0, bb = 0;
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-          a += tab.M[q * N + i] * u[i];
-          bb += tab.Kx[q * N + i] * u[i];
-        }
-        ao[q] = a;
-        bo[q] = bb;
-      }
-    }
-    __syncthreads();
-
-    // ---- y sweep (in place): c = M a, de = Ky a + M b
-    for (int w = tid; w < ncell * N * N; w += NT) {
-      const int cell = w / (N * N);
-      const int rr = w - cell * (N * N);
-      const int k = rr / N, i = rr - k * N;
-      T* ac = A + cell * TILE + k * N * RS + i;
-      T* bc = Bs + cell * TILE + k * N * RS + i;
-      T a[N], bb[N];
-#pragma unroll
-      for (int j = 0; j < N; ++j) { a[j] = ac[j * RS]; bb[j] = bc[j * RS]; }
-#pragma unroll
-      for (int q = 0; q < N; ++q) {
-        T c = 0, de = 0;
-#pragma unroll
-        for (int j = 0; j < N; ++j) {
-          c += tab.M[q * N + j] * a[j];
-          de += tab.Ky[q * N + j] * a[j];
-        }
-#pragma unroll
-        for (int j = 0; j < N; ++j) de += tab.M[q * N + j] * bb[j];
-        ac[q * RS] = c;
-        bc[q * RS] = de;
-      }
-    }
-    __syncthreads();
-
-    // ---- z sweep: out = M de + Kz c, written over c
-    for (int w = tid; w < ncell * N * N; w += NT) {
-      const int cell = w / (N * N);
-      const int rr = w - cell * (N * N);
-      const int j = rr / N, i = rr - j * N;
-      T* ac = A + cell * TILE + j * RS + i;
-      const T* bc = Bs + cell * TILE + j * RS + i;
-      T c[N], de[N];
-#pragma unroll
-      for (int k = 0; k < N; ++k) { c[k] = ac[k * N * RS]; de[k] = bc[k * N * RS]; }
-#pragma unroll
-      for (int q = 0; q < N; ++q) {
-        T o = 0;
-#pragma unroll
-        for (int k = 0; k < N; ++k) o += tab.M[q * N + k] * de[k];
-#pragma unroll
-        for (int k = 0; k < N; ++k) o += tab.Kz[q * N + k] * c[k];
-        ac[q * N * RS] = o;
-      }
-    }
-    __syncthreads();
-
-    // ---- gather the cells' contributions per lattice point, finish the planes
-    for (int rem = tid; rem < fp; rem += NT) {
-      const int j = (int)(((unsigned)rem * fw_magic) >> 16);
-      const int i = rem - j * fw;
-      const int ex = i == 0 ? 0 : (i == Lx ? 2 : 1), ey = j == 0 ? 0 : (j == Ly ? 2 : 1);
-      const int ox = ex == 1 ? i - 1 : 0, oy = ey == 1 ? j - 1 : 0;
-      const int lx = ex == 1 ? Lx - 1 : 1, ly = ey == 1 ? Ly - 1 : 1;
-      const bool edge = (ex != 1) || (ey != 1);
-      int cx1 = i / P;
-      const int ix1 = i - cx1 * P;
-      const int cx0 = (ix1 == 0 && cx1 > 0) ? cx1 - 1 : -1;
-      if (cx1 >= bcx) cx1 = -1;
-      int cy1 = j / P;
-      const int iy1 = j - cy1 * P;
-      const int cy0 = (iy1 == 0 && cy1 > 0) ? cy1 - 1 : -1;
-      if (cy1 >= bcy) cy1 = -1;
-      // offsets of the (up to four) cell-tile entries holding this point
-      const int o11 = (cy1 >= 0 && cx1 >= 0) ? (cy1 * bcx + cx1) * TILE + iy1 * RS + ix1 : -1;
-      const int o10 = (cy1 >= 0 && cx0 >= 0) ? (cy1 * bcx + cx0) * TILE + iy1 * RS + P : -1;
-      const int o01 = (cy0 >= 0 && cx1 >= 0) ? (cy0 * bcx + cx1) * TILE + P * RS + ix1 : -1;
-      const int o00 = (cy0 >= 0 && cx0 >= 0) ? (cy0 * bcx + cx0) * TILE + P * RS + P : -1;
-#pragma unroll
-      for (int k = 0; k <= P; ++k) {
-        T sum = 0;
-        if (o00 >= 0) sum += A[o00 + k * N * RS];
-        if (o01 >= 0) sum += A[o01 + k * N * RS];
-        if (o10 >= 0) sum += A[o10 + k * N * RS];
-        if (o11 >= 0) sum += A[o11 + k * N * RS];
-        if (k == 0) sum += carry[j * WX + i];
-        if (k == P && kz < bcz - 1) {
-          carry[j * WX + i] = sum;
-          Pw[j * WX + i] = Pw[P * PLANE + j * WX + i];
-          continue;
-        }
-        const int K = kz * P + k;
-        const int ez = K == 0 ? 0 : (K == Lz ? 2 : 1);
-        const int oz = ez == 1 ? K - 1 : 0;
-        const i64 gi = st27[ex + 3 * ey + 9 * ez] + ox + (i64)lx * (oy + ly * oz);
-        if (!(edge || ez != 1)) {
-          V[gi] = sum;
-          if (MODE == 1) {
-            const double r = (double)R[gi], m = (double)Minv[gi];
-            const double p = (double)Pw[k * PLANE + j * WX + i], v = (double)sum;
+          for (int c = 0; c < P; ++c) {
+            const int K = Klo + c;
+            if (K > Khi) break;
+            const i64 gi = base + pstride * (K - 1);
+            const double r = (double)R[gi], m = (double)Minv[gi], p = (double)Pv[gi], v = (double)V[gi];
             const double mr = m * r, mv = m * v;
             s[0] += r * r; s[1] += p * v; s[2] += r * v; s[3] += v * v;
             s[4] += r * mr; s[5] += r * mv; s[6] += v * mv;
           }
-        } else if (!g.mask[gi - n_int]) {
-          atomicAdd(&V[gi], sum);
         }
       }
     }
-    // next layer's loads are ordered after this gather by the barrier that
-    // follows them; Pw[1..P] is only rewritten by the thread that just read it
+  } else {
+    // ===================== math warps =====================
+    const int ncell = bcx * bcy;
+    const unsigned bcx_magic = (65536u + bcx - 1) / bcx;
+    for (int L = 0; L < bcz; ++L) {
+      const int stage = L & 1;
+      const int s0 = (L * P) % RB;
+      if (L > 0) math_barrier<NT_C>();        // every math thread is done with the previous gather's tiles
+      mbar_wait(&bars[stage], (L >> 1) & 1);  // layer L full
+
+      // ---- x sweep: a = M u, b = gx K u along every x line of every cell
+      for (int w = tid; w < ncell * N * N; w += NT_C) {
+        const int cell = w / (N * N);
+        const int rr = w - cell * (N * N);
+        const int k = rr / N, j = rr - k * N;
+        const int cy = (int)(((unsigned)cell * bcx_magic) >> 16);
+        const int cx = cell - cy * bcx;
+        int slot = s0 + k;
+        if (slot >= RB) slot -= RB;
+        const T* row = ring + slot * PLANE + (cy * P + j) * WX + cx * P;
+        T u[N], e[HE], o[HE];
+#pragma unroll
+        for (int i = 0; i < N; ++i) u[i] = row[i];
+        eo_split<N>(u, e, o);
+        T* ao = A + cell * TILE + (k * N + j) * RS;
+        T* bo = Bs + cell * TILE + (k * N + j) * RS;
+        T se[HE], so[HE], te[HE], to[HE], out[N];
+#pragma unroll
+        for (int i = 0; i < HE; ++i) { se[i] = 0; so[i] = 0; te[i] = 0; to[i] = 0; }
+        eo_mul<N>(tab.Me, tab.Mo, e, o, se, so);
+        eo_mul<N>(tab.Ke, tab.Ko, e, o, te, to);
+        eo_join<N>(se, so, out);
+#pragma unroll
+        for (int q = 0; q < N; ++q) ao[q] = out[q];
+#pragma unroll
+        for (int i = 0; i < HE; ++i) { te[i] *= tab.g[0]; to[i] *= tab.g[0]; }
+        eo_join<N>(te, to, out);
+#pragma unroll
+        for (int q = 0; q < N; ++q) bo[q] = out[q];
+      }
+      math_barrier<NT_C>();
+
+      // ---- y sweep (in place): c = M a, de = gy K a + M b
+      for (int w = tid; w < ncell * N * N; w += NT_C) {
+        const int cell = w / (N * N);
+        const int rr = w - cell * (N * N);
+        const int k = rr / N, i = rr - k * N;
+        T* ac = A + cell * TILE + k * N * RS + i;
+        T* bc = Bs + cell * TILE + k * N * RS + i;
+        T a[N], bb[N], ea[HE], oa[HE], eb[HE], ob[HE];
+#pragma unroll
+        for (int j = 0; j < N; ++j) { a[j] = ac[j * RS]; bb[j] = bc[j * RS]; }
+        eo_split<N>(a, ea, oa);
+        eo_split<N>(bb, eb, ob);
+        T se[HE], so[HE], te[HE], to[HE], out[N];
+#pragma unroll
+        for (int i2 = 0; i2 < HE; ++i2) { se[i2] = 0; so[i2] = 0; te[i2] = 0; to[i2] = 0; }
+        eo_mul<N>(tab.Me, tab.Mo, ea, oa, se, so);  // c = M a
+        eo_join<N>(se, so, out);
+#pragma unroll
+        for (int q = 0; q < N; ++q) ac[q * RS] = out[q];
+        eo_mul<N>(tab.Ke, tab.Ko, ea, oa, te, to);  // K a
+#pragma unroll
+        for (int i2 = 0; i2 < HE; ++i2) { se[i2] = 0; so[i2] = 0; }
+        eo_mul<N>(tab.Me, tab.Mo, eb, ob, se, so);  // M b
+#pragma unroll
+        for (int i2 = 0; i2 < HE; ++i2) { se[i2] += tab.g[1] * te[i2]; so[i2] += tab.g[1] * to[i2]; }
+        eo_join<N>(se, so, out);
+#pragma unroll
+        for (int q = 0; q < N; ++q) bc[q * RS] = out[q];
+      }
+      math_barrier<NT_C>();
+
+      // ---- z sweep: out = M de + gz K c, written over c
+      for (int w = tid; w < ncell * N * N; w += NT_C) {
+        const int cell = w / (N * N);
+        const int rr = w - cell * (N * N);
+        const int j = rr / N, i = rr - j * N;
+        T* ac = A + cell * TILE + j * RS + i;
+        const T* bc = Bs + cell * TILE + j * RS + i;
+        T c[N], de[N], ec[HE], oc[HE], ed[HE], od[HE];
+#pragma unroll
+        for (int k = 0; k < N; ++k) { c[k] = ac[k * N * RS]; de[k] = bc[k * N * RS]; }
+        eo_split<N>(c, ec, oc);
+        eo_split<N>(de, ed, od);
+        T se[HE], so[HE], te[HE], to[HE], out[N];
+#pragma unroll
+        for (int i2 = 0; i2 < HE; ++i2) { se[i2] = 0; so[i2] = 0; te[i2] = 0; to[i2] = 0; }
+        eo_mul<N>(tab.Ke, tab.Ko, ec, oc, te, to);  // K c
+        eo_mul<N>(tab.Me, tab.Mo, ed, od, se, so);  // M de
+#pragma unroll
+        for (int i2 = 0; i2 < HE; ++i2) { se[i2] += tab.g[2] * te[i2]; so[i2] += tab.g[2] * to[i2]; }
+        eo_join<N>(se, so, out);
+#pragma unroll
+        for (int q = 0; q < N; ++q) ac[q * N * RS] = out[q];
+      }
+      math_barrier<NT_C>();
+
+      // ---- gather the cells' contributions per lattice point, finish the planes
+      for (int rem = tid; rem < fp; rem += NT_C) {
+        const int j = (int)(((unsigned)rem * fw_magic) >> 16);
+        const int i = rem - j * fw;
+        const int ex = i == 0 ? 0 : (i == Lx ? 2 : 1), ey = j == 0 ? 0 : (j == Ly ? 2 : 1);
+        const int ox = ex == 1 ? i - 1 : 0, oy = ey == 1 ? j - 1 : 0;
+        const int lx = ex == 1 ? Lx - 1 : 1, ly = ey == 1 ? Ly - 1 : 1;
+        const bool edge = (ex != 1) || (ey != 1);
+        const int e2 = ex + 3 * ey, o2 = ox + lx * oy, pstride = lx * ly;
+        int cx1 = i / P;
+        const int ix1 = i - cx1 * P;
+        const int cx0 = (ix1 == 0 && cx1 > 0) ? cx1 - 1 : -1;
+        if (cx1 >= bcx) cx1 = -1;
+        int cy1 = j / P;
+        const int iy1 = j - cy1 * P;
+        const int cy0 = (iy1 == 0 && cy1 > 0) ? cy1 - 1 : -1;
+        if (cy1 >= bcy) cy1 = -1;
+        // offsets of the (up to four) cell-tile entries holding this point
+        const int o11 = (cy1 >= 0 && cx1 >= 0) ? (cy1 * bcx + cx1) * TILE + iy1 * RS + ix1 : -1;
+        const int o10 = (cy1 >= 0 && cx0 >= 0) ? (cy1 * bcx + cx0) * TILE + iy1 * RS + P : -1;
+        const int o01 = (cy0 >= 0 && cx1 >= 0) ? (cy0 * bcx + cx1) * TILE + P * RS + ix1 : -1;
+        const int o00 = (cy0 >= 0 && cx0 >= 0) ? (cy0 * bcx + cx0) * TILE + P * RS + P : -1;
+#pragma unroll
+        for (int k = 0; k <= P; ++k) {
+          T sum = 0;
+          if (o00 >= 0) sum += A[o00 + k * N * RS];
+          if (o01 >= 0) sum += A[o01 + k * N * RS];
+          if (o10 >= 0) sum += A[o10 + k * N * RS];
+          if (o11 >= 0) sum += A[o11 + k * N * RS];
+          if (k == 0) sum += carry[j * WX + i];
+          if (k == P && L < bcz - 1) {
+            carry[j * WX + i] = sum;
+            continue;
+          }
+          const int K = L * P + k;
+          const int ez = K == 0 ? 0 : (K == Lz ? 2 : 1);
+          const i64 gi = st27[e2 + 9 * ez] + o2 + (ez == 1 ? (i64)pstride * (K - 1) : 0);
+          // constrained rows receive garbage here; k_post / k_surface_fix restore v_c = p_c
+          if (!(edge || ez != 1)) V[gi] = sum;
+          else atomicAdd(&V[gi], sum);
+        }
+      }
+      mbar_arrive(&bars[2 + stage]);  // layer L consumed (orders the v stores before the post loads)
+    }
   }
-  if (MODE == 1) block_reduce7_store(s, red, partials + (i64)blockIdx.x * 8);
+  if (MODE == 1) {
+    // block sum of the memory warps' partial sums (math warps contribute zeros)
+    __syncthreads();
+    block_reduce7_store(s, red, partials + (i64)blockIdx.x * 8);
+  }
 }
 
 // ---------------------------------------------------------------------------
 // Range kernels over [lo, hi) in brick numbering.
 
-// dst[i] = constrained ? src[i] : 0 on the shared range (operator.py:334-335, 359-360)
+// dst = 0 on the shared range before the atomic accumulation (operator.py:334-335)
 template <typename T>
-__global__ void k_surface_init(BrickGrid g, const T* __restrict__ src, T* __restrict__ dst) {
+__global__ void k_surface_init(BrickGrid g, T* __restrict__ dst) {
   const i64 n_sh = g.n_dofs - g.n_int;
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n_sh; i += (i64)gridDim.x * blockDim.x)
-    dst[g.n_int + i] = g.mask[i] ? src[g.n_int + i] : (T)0;
+    dst[g.n_int + i] = (T)0;
 }
 
-// merged-CG "pre" (solvers.py:660-690); with init_v also resets v for the
-// atomic accumulation: constrained rows are identity, v_c = p_c.
+// constrained rows are identity: dst[c] = src[c] (operator.py:359-360)
+template <typename T>
+__global__ void k_surface_fix(BrickGrid g, const T* __restrict__ src, T* __restrict__ dst) {
+  const i64 n_sh = g.n_dofs - g.n_int;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n_sh; i += (i64)gridDim.x * blockDim.x)
+    if (g.mask[i]) dst[g.n_int + i] = src[g.n_int + i];
+}
+
+// merged-CG "pre" (solvers.py:660-690); with init_v also zeroes v for the
+// atomic accumulation of the brick kernel.
 template <typename T>
 __global__ void k_pre(BrickGrid g, i64 lo, i64 hi, int init_v, T* __restrict__ R, T* __restrict__ Pv,
                       T* __restrict__ V, T* __restrict__ X, const T* __restrict__ Minv,
@@ -373,20 +537,25 @@ __global__ void k_pre(BrickGrid g, i64 lo, i64 hi, int init_v, T* __restrict__ R
     p = m * r + bm1 * p;
     R[i] = r;
     Pv[i] = p;
-    if (init_v) V[i] = (i >= g.n_int && g.mask[i - g.n_int]) ? p : (T)0;
+    if (init_v) V[i] = (T)0;
   }
 }
 
 // merged-CG "post": the seven sums (solvers.py:112-127, 692-698)
 template <typename T>
-__global__ void k_post(i64 lo, i64 hi, const T* __restrict__ R, const T* __restrict__ Pv,
-                       const T* __restrict__ V, const T* __restrict__ Minv,
+__global__ void k_post(BrickGrid g, i64 lo, i64 hi, int fix_constrained, const T* __restrict__ R,
+                       const T* __restrict__ Pv, T* __restrict__ V, const T* __restrict__ Minv,
                        const SolveState* __restrict__ st, double* __restrict__ partials) {
   __shared__ double red[7 * 32];
   if (!st->active) return;
   double s[7] = {0, 0, 0, 0, 0, 0, 0};
   for (i64 i = lo + blockIdx.x * (i64)blockDim.x + threadIdx.x; i < hi; i += (i64)gridDim.x * blockDim.x) {
-    const double r = (double)R[i], p = (double)Pv[i], v = (double)V[i], m = (double)Minv[i];
+    const double r = (double)R[i], p = (double)Pv[i], m = (double)Minv[i];
+    double v = (double)V[i];
+    if (fix_constrained && i >= g.n_int && g.mask[i - g.n_int]) {  // identity row: v_c = p_c
+      v = p;
+      V[i] = (T)p;
+    }
     const double mr = m * r, mv = m * v;
     s[0] += r * r; s[1] += p * v; s[2] += r * v; s[3] += v * v;
     s[4] += r * mr; s[5] += r * mv; s[6] += v * mv;
