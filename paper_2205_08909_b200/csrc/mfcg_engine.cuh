@@ -474,6 +474,19 @@ int Engine<P, T>::solve(const mfcg_solve_args* a, mfcg_solve_result* res) {
     }
     res->operator_ms = acc;
   }
+#ifdef MFCG_TIMING
+  {
+    unsigned long long h[16];
+    cudaMemcpyFromSymbol(h, g_phase_cycles, sizeof(h));
+    const char* names[16] = {"P.wait_empty", "P.fill", "P.post", "", "C.wait_full", "C.x", "C.y", "C.z", "C.bar", "C.gather",
+                             "", "", "", "", "", ""};
+    std::fprintf(stderr, "[mfcg timing] warp-cycles summed over all warps and launches (op launches %lld):\n", (long long)op_launches_);
+    for (int i = 0; i < 10; ++i)
+      if (names[i][0]) std::fprintf(stderr, "  %-14s %14llu\n", names[i], h[i]);
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+  }
+#endif
   res->kernel_launches = launches_;
   res->operator_launches = op_launches_;
   res->iterations = s.k;

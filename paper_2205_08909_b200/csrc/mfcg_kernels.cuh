@@ -24,6 +24,15 @@ namespace mfcg {
 
 typedef long long i64;
 
+#ifdef MFCG_TIMING
+static __device__ unsigned long long g_phase_cycles[16];
+#define MFCG_TIC(var) long long var = clock64()
+#define MFCG_TOC(var, slot) do { long long now__ = clock64(); if ((threadIdx.x & 31) == 0) atomicAdd(&g_phase_cycles[slot], (unsigned long long)(now__ - var)); var = now__; } while (0)
+#else
+#define MFCG_TIC(var)
+#define MFCG_TOC(var, slot)
+#endif
+
 struct BrickGrid {
   int p;
   int cells[3];   // cells of this rank's mesh (slab)
@@ -53,21 +62,21 @@ struct SolveState {
 // Per-degree launch shape of the brick kernel: BX x BY cells per brick layer,
 // NT_C "math" threads (sum-factorisation sweeps, shared memory only), NT_P
 // "memory" threads (all global loads: pre on the way in, post one layer behind),
-// KC lattice planes per load batch (memory-level parallelism per thread).
+// KC points per load batch of a memory thread (memory-level parallelism).
 template <int P> struct Cfg;
 #define MFCG_CFG(P_, B_, TC_, TP_, KC_, MB_)                                                   \
   template <> struct Cfg<P_> {                                                                 \
     static constexpr int BX = B_, BY = B_, NT_C = TC_, NT_P = TP_, KC = KC_, MINB = MB_,       \
                          THREADS = TC_ + TP_;                                                  \
   };
-MFCG_CFG(1, 16, 256, 128, 2, 2)
-MFCG_CFG(2, 10, 256, 128, 3, 2)
-MFCG_CFG(3, 6, 192, 128, 4, 2)
-MFCG_CFG(4, 5, 224, 128, 3, 2)
-MFCG_CFG(5, 4, 192, 128, 3, 2)
-MFCG_CFG(6, 3, 224, 128, 3, 2)
-MFCG_CFG(7, 2, 128, 128, 4, 2)
-MFCG_CFG(8, 2, 128, 128, 3, 2)
+MFCG_CFG(1, 16, 256, 256, 3, 2)
+MFCG_CFG(2, 10, 256, 256, 3, 2)
+MFCG_CFG(3, 6, 192, 320, 3, 2)
+MFCG_CFG(4, 5, 224, 288, 3, 2)
+MFCG_CFG(5, 4, 192, 320, 3, 2)
+MFCG_CFG(6, 3, 224, 288, 3, 2)
+MFCG_CFG(7, 2, 128, 256, 3, 2)
+MFCG_CFG(8, 2, 128, 256, 3, 2)
 
 template <int P> struct Geo {
   static constexpr int N = P + 1;
@@ -247,114 +256,173 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, const T* __restrict__ src, T* __re
   const int fw = Lx + 1, fp = fw * (Ly + 1);
   const unsigned fw_magic = (65536u + fw - 1) / fw;
   const i64 n_int = g.n_int;
-  double s[7] = {0, 0, 0, 0, 0, 0, 0};
 
   if (tid >= NT_C) {
     // ===================== memory warps =====================
     const int ptid = tid - NT_C;
+    const int pwarp = ptid >> 5;
+    const int nint2d = (Lx - 1) * (Ly - 1);                  // interior points of one lattice plane
+    const int nperim = fp - nint2d;                           // brick-boundary points of one plane
+    const int lxm = Lx > 1 ? Lx - 1 : 1;
+    const unsigned lxm_magic = (65536u + lxm - 1) / lxm;
+    const unsigned n2d_magic = nint2d > 0 ? (unsigned)((0x100000000ull + nint2d - 1) / nint2d) : 0u;
+    const unsigned per_magic = (unsigned)((0x100000000ull + nperim - 1) / nperim);
+    const i64 st_int = st27[13];
+    if ((ptid & 31) == 0)
+      for (int q = 0; q < 7; ++q) red[pwarp * 7 + q] = 0.0;
+    MFCG_TIC(tp);
     for (int L = 0; L < bcz + 2; ++L) {
       const int stage = L & 1;
       if (L >= 2) mbar_wait(&bars[2 + stage], ((L >> 1) - 1) & 1);  // layer L-2 consumed
+      MFCG_TOC(tp, 0);
       if (L < bcz) {
         // ---- fill the ring with the planes layer L adds (plane 0 is shared with layer L-1)
         const int k0 = L == 0 ? 0 : 1;
-        const int s0 = (L * P) % RB;
-        for (int rem = ptid; rem < fp; rem += NT_P) {
-          const int j = (int)(((unsigned)rem * fw_magic) >> 16);
-          const int i = rem - j * fw;
-          const int ex = i == 0 ? 0 : (i == Lx ? 2 : 1), ey = j == 0 ? 0 : (j == Ly ? 2 : 1);
-          const int ox = ex == 1 ? i - 1 : 0, oy = ey == 1 ? j - 1 : 0;
-          const int lx = ex == 1 ? Lx - 1 : 1, ly = ey == 1 ? Ly - 1 : 1;
-          const bool edge = (ex != 1) || (ey != 1);
-          const int e2 = ex + 3 * ey, o2 = ox + lx * oy, pstride = lx * ly;
-          T* rp = ring + j * WX + i;
+        // (a) brick-interior points: one contiguous run per vector, pre fused (solvers.py:660-690)
+        const int Kfirst = L * P + k0 > 1 ? L * P + k0 : 1;
+        const int Klast = L * P + P < Lz - 1 ? L * P + P : Lz - 1;
+        const int nitem = (nint2d > 0 && Klast >= Kfirst) ? (Klast - Kfirst + 1) * nint2d : 0;
+        const i64 gbase = st_int + (i64)nint2d * (Kfirst - 1);
+        for (int it0 = ptid; it0 < nitem; it0 += KC * NT_P) {
+          T rr[KC], vv[KC], pp[KC], mm[KC], xx[KC];
 #pragma unroll
-          for (int kb = 0; kb <= P; kb += KC) {
-            i64 gi[KC];
-            bool sh[KC], on[KC];
-            unsigned char mk[KC];
-            T rr[KC], vv[KC], pp[KC], mm[KC], xx[KC];
-            // issue every load of the batch before any value is used: no load may
-            // depend on loaded data, or the warp pays one DRAM round trip per plane
+          for (int c = 0; c < KC; ++c) {
+            const int it = it0 + c * NT_P;
+            rr[c] = vv[c] = pp[c] = mm[c] = xx[c] = (T)0;
+            if (it < nitem) {
+              const i64 gi = gbase + it;
+              if (MODE == 0) {
+                pp[c] = src[gi];
+              } else {
+                pp[c] = Pv[gi]; rr[c] = R[gi]; vv[c] = V[gi]; mm[c] = Minv[gi];
+                if (xmode) xx[c] = X[gi];
+              }
+            }
+          }
 #pragma unroll
-            for (int c = 0; c < KC; ++c) {
-              const int k = kb + c;
-              on[c] = k <= P && k >= k0;
-              const int K = L * P + k;
-              const int ez = K == 0 ? 0 : (K == Lz ? 2 : 1);
-              gi[c] = st27[e2 + 9 * ez] + o2 + (ez == 1 ? (i64)pstride * (K - 1) : 0);
-              sh[c] = edge || ez != 1;
-              rr[c] = vv[c] = mm[c] = xx[c] = pp[c] = (T)0;
-              mk[c] = 0;
-              if (on[c]) {
-                pp[c] = MODE == 0 ? src[gi[c]] : Pv[gi[c]];
-                if (sh[c]) {
-                  mk[c] = g.mask[gi[c] - n_int];
-                } else if (MODE == 1) {
-                  rr[c] = R[gi[c]]; vv[c] = V[gi[c]]; mm[c] = Minv[gi[c]];
-                  if (xmode) xx[c] = X[gi[c]];
-                }
+          for (int c = 0; c < KC; ++c) {
+            const int it = it0 + c * NT_P;
+            if (it >= nitem) continue;
+            T val = pp[c];
+            if (MODE == 1) {
+              const i64 gi = gbase + it;
+              T r = rr[c], p = pp[c];
+              if (xmode) {
+                T x = xx[c];
+                if (xmode == 2) x += xc1 * p + xc2 * (p - mm[c] * r);
+                else x += xc1 * p;
+                X[gi] = x;
+              }
+              r -= am1 * vv[c];
+              p = mm[c] * r + bm1 * p;
+              R[gi] = r;
+              Pv[gi] = p;
+              val = p;
+            }
+            const int kk = (int)__umulhi((unsigned)it, n2d_magic);
+            const int rem2 = it - kk * nint2d;
+            const int jm = (int)(((unsigned)rem2 * lxm_magic) >> 16);
+            const int im = rem2 - jm * lxm;
+            ring[((Kfirst + kk) % RB) * PLANE + (jm + 1) * WX + im + 1] = val;
+          }
+        }
+        // (b) brick-boundary points of the layer's planes: already pre-updated by k_pre; p only
+        {
+          const int nk = P + 1 - k0;
+          const int nsh = nk * nperim;
+          for (int it0 = ptid; it0 < nsh; it0 += 2 * NT_P) {
+            T pp[2];
+            unsigned char mk[2];
+            int dst[2];
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              const int it = it0 + c * NT_P;
+              pp[c] = (T)0; mk[c] = 0; dst[c] = -1;
+              if (it < nsh) {
+                const int kk = (int)__umulhi((unsigned)it, per_magic);
+                const int e = it - kk * nperim;
+                int i, j;
+                if (e < fw) { j = 0; i = e; }
+                else if (e < 2 * fw) { j = Ly; i = e - fw; }
+                else { const int r2 = e - 2 * fw; j = 1 + (r2 >> 1); i = (r2 & 1) ? Lx : 0; }
+                const int ex = i == 0 ? 0 : (i == Lx ? 2 : 1), ey = j == 0 ? 0 : (j == Ly ? 2 : 1);
+                const int ox = ex == 1 ? i - 1 : 0, oy = ey == 1 ? j - 1 : 0;
+                const int lx = ex == 1 ? Lx - 1 : 1, ly = ey == 1 ? Ly - 1 : 1;
+                const int K = L * P + k0 + kk;
+                const int ez = K == 0 ? 0 : (K == Lz ? 2 : 1);
+                const i64 gi = st27[ex + 3 * ey + 9 * ez] + ox + lx * oy + (ez == 1 ? (i64)(lx * ly) * (K - 1) : 0);
+                pp[c] = MODE == 0 ? src[gi] : Pv[gi];
+                mk[c] = g.mask[gi - n_int];
+                dst[c] = (K % RB) * PLANE + j * WX + i;
               }
             }
 #pragma unroll
-            for (int c = 0; c < KC; ++c) {
-              const int k = kb + c;
-              if (!on[c]) continue;
-              T val = mk[c] ? (T)0 : pp[c];
-              if (MODE == 1 && !sh[c]) {
-                T r = rr[c], p = pp[c];
-                if (xmode) {
-                  T x = xx[c];
-                  if (xmode == 2) x += xc1 * p + xc2 * (p - mm[c] * r);
-                  else x += xc1 * p;
-                  X[gi[c]] = x;
-                }
-                r -= am1 * vv[c];
-                p = mm[c] * r + bm1 * p;
-                R[gi[c]] = r;
-                Pv[gi[c]] = p;
-                val = p;
-              }
-              int slot = s0 + k;
-              if (slot >= RB) slot -= RB;
-              rp[slot * PLANE] = val;
-            }
+            for (int c = 0; c < 2; ++c)
+              if (dst[c] >= 0) ring[dst[c]] = mk[c] ? (T)0 : pp[c];
+          }
+        }
+        // (c) the brick's bottom / top face interiors (first / last layer only): contiguous
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+          if (side == 0 ? (L != 0) : (L != bcz - 1)) continue;
+          const i64 fb = st27[side == 0 ? 4 : 22];
+          const int slot = ((side == 0 ? 0 : Lz) % RB) * PLANE;
+          for (int it = ptid; it < nint2d; it += NT_P) {
+            const T pv = MODE == 0 ? src[fb + it] : Pv[fb + it];
+            const unsigned char mk = g.mask[fb + it - n_int];
+            const int jm = (int)(((unsigned)it * lxm_magic) >> 16);
+            const int im = it - jm * lxm;
+            ring[slot + (jm + 1) * WX + im + 1] = mk ? (T)0 : pv;
           }
         }
         mbar_arrive(&bars[stage]);  // layer L full
+        MFCG_TOC(tp, 1);
       }
       if (MODE == 1 && L >= 2) {
-        // ---- post sums of layer L-2 (its v is final and, like r, p, 1/diag, still in L2)
+        // ---- post sums of layer L-2 (solvers.py:692-698): its v is final and, like r, p and
+        // 1/diag, still resident in L2; one contiguous run per vector
         const int Lp = L - 2;
-        const int Klo = Lp == 0 ? 1 : Lp * P, Khi = Lp * P + P - 1;  // interior planes finished by layer Lp
-        for (int rem = ptid; rem < fp; rem += NT_P) {
-          const int j = (int)(((unsigned)rem * fw_magic) >> 16);
-          const int i = rem - j * fw;
-          if (i == 0 || i == Lx || j == 0 || j == Ly) continue;
-          const i64 base = st27[13] + (i - 1) + (i64)(Lx - 1) * (j - 1);
-          const i64 pstride = (i64)(Lx - 1) * (Ly - 1);
+        const int Klo = Lp == 0 ? 1 : Lp * P, Khi = Lp * P + P - 1;
+        const int nitem = nint2d > 0 ? (Khi - Klo + 1) * nint2d : 0;
+        const i64 gbase = st_int + (i64)nint2d * (Klo - 1);
+        double s[7] = {0, 0, 0, 0, 0, 0, 0};
+        for (int it0 = ptid; it0 < nitem; it0 += KC * NT_P) {
+          T rr[KC], vv[KC], pp[KC], mm[KC];
 #pragma unroll
-          for (int c = 0; c < P; ++c) {
-            const int K = Klo + c;
-            if (K > Khi) break;
-            const i64 gi = base + pstride * (K - 1);
-            const double r = (double)R[gi], m = (double)Minv[gi], p = (double)Pv[gi], v = (double)V[gi];
+          for (int c = 0; c < KC; ++c) {
+            const int it = it0 + c * NT_P;
+            rr[c] = vv[c] = pp[c] = mm[c] = (T)0;
+            if (it < nitem) {
+              const i64 gi = gbase + it;
+              rr[c] = R[gi]; vv[c] = V[gi]; pp[c] = Pv[gi]; mm[c] = Minv[gi];
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < KC; ++c) {
+            const double r = (double)rr[c], m = (double)mm[c], p = (double)pp[c], v = (double)vv[c];
             const double mr = m * r, mv = m * v;
             s[0] += r * r; s[1] += p * v; s[2] += r * v; s[3] += v * v;
             s[4] += r * mr; s[5] += r * mv; s[6] += v * mv;
           }
         }
+        warp_reduce7(s);
+        if ((ptid & 31) == 0)
+#pragma unroll
+          for (int q = 0; q < 7; ++q) red[pwarp * 7 + q] += s[q];
+        MFCG_TOC(tp, 2);
       }
     }
   } else {
     // ===================== math warps =====================
     const int ncell = bcx * bcy;
     const unsigned bcx_magic = (65536u + bcx - 1) / bcx;
+    MFCG_TIC(tc);
     for (int L = 0; L < bcz; ++L) {
       const int stage = L & 1;
       const int s0 = (L * P) % RB;
       if (L > 0) math_barrier<NT_C>();        // every math thread is done with the previous gather's tiles
       mbar_wait(&bars[stage], (L >> 1) & 1);  // layer L full
+      MFCG_TOC(tc, 4);
 
       // ---- x sweep: a = M u, b = gx K u along every x line of every cell
       for (int w = tid; w < ncell * N * N; w += NT_C) {
@@ -386,7 +454,9 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, const T* __restrict__ src, T* __re
 #pragma unroll
         for (int q = 0; q < N; ++q) bo[q] = out[q];
       }
+      MFCG_TOC(tc, 5);
       math_barrier<NT_C>();
+      MFCG_TOC(tc, 8);
 
       // ---- y sweep (in place): c = M a, de = gy K a + M b
       for (int w = tid; w < ncell * N * N; w += NT_C) {
@@ -417,7 +487,9 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, const T* __restrict__ src, T* __re
 #pragma unroll
         for (int q = 0; q < N; ++q) bc[q * RS] = out[q];
       }
+      MFCG_TOC(tc, 6);
       math_barrier<NT_C>();
+      MFCG_TOC(tc, 8);
 
       // ---- z sweep: out = M de + gz K c, written over c
       for (int w = tid; w < ncell * N * N; w += NT_C) {
@@ -442,7 +514,9 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, const T* __restrict__ src, T* __re
 #pragma unroll
         for (int q = 0; q < N; ++q) ac[q * N * RS] = out[q];
       }
+      MFCG_TOC(tc, 7);
       math_barrier<NT_C>();
+      MFCG_TOC(tc, 8);
 
       // ---- gather the cells' contributions per lattice point, finish the planes
       for (int rem = tid; rem < fp; rem += NT_C) {
@@ -487,12 +561,17 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, const T* __restrict__ src, T* __re
         }
       }
       mbar_arrive(&bars[2 + stage]);  // layer L consumed (orders the v stores before the post loads)
+      MFCG_TOC(tc, 9);
     }
   }
   if (MODE == 1) {
-    // block sum of the memory warps' partial sums (math warps contribute zeros)
+    // block sums: the memory warps' slots, added in a fixed order (deterministic)
     __syncthreads();
-    block_reduce7_store(s, red, partials + (i64)blockIdx.x * 8);
+    if (tid < 7) {
+      double acc = 0.0;
+      for (int w = 0; w < NT_P / 32; ++w) acc += red[w * 7 + tid];
+      partials[(i64)blockIdx.x * 8 + tid] = acc;
+    }
   }
 }
 
