@@ -164,9 +164,10 @@ class Engine : public EngineBase {
 
   int ensure_vectors(bool all) {
     const i64 n = c_->grid.n_dofs;
-    for (T** v : {&p_, &v_}) if (!*v) MFCG_CUDA(cudaMalloc(v, sizeof(T) * n));
+    // +32 bytes: the brick kernel reads whole aligned 16-byte chunks
+    for (T** v : {&p_, &v_}) if (!*v) MFCG_CUDA(cudaMalloc(v, sizeof(T) * n + 32));
     if (all)
-      for (T** v : {&x_, &r_, &z_, &minv_}) if (!*v) MFCG_CUDA(cudaMalloc(v, sizeof(T) * n));
+      for (T** v : {&x_, &r_, &z_, &minv_}) if (!*v) MFCG_CUDA(cudaMalloc(v, sizeof(T) * n + 32));
     return MFCG_OK;
   }
 
@@ -480,7 +481,7 @@ int Engine<P, T>::solve(const mfcg_solve_args* a, mfcg_solve_result* res) {
     cudaMemcpyFromSymbol(h, g_phase_cycles, sizeof(h));
     const char* names[16] = {"P.wait_empty", "P.fill", "P.post", "", "C.wait_full", "C.x", "C.y", "C.z", "C.bar", "C.gather",
                              "", "", "", "", "", ""};
-    std::fprintf(stderr, "[mfcg timing] warp-cycles summed over all warps and launches (op launches %lld):\n", (long long)op_launches_);
+    std::fprintf(stderr, "[mfcg timing] cycles of one warp per role summed over blocks and launches (op launches %lld):\n", (long long)op_launches_);
     for (int i = 0; i < 10; ++i)
       if (names[i][0]) std::fprintf(stderr, "  %-14s %14llu\n", names[i], h[i]);
     unsigned long long z[16] = {0};

@@ -20,14 +20,27 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#ifndef MFCG_SKIP
+#define MFCG_SKIP 0  // debug only: 1 skip sweeps, 2 skip gather, 4 skip post, 8 skip fill loads
+#endif
+
 namespace mfcg {
 
 typedef long long i64;
 
 #ifdef MFCG_TIMING
+// Light phase timing: one designated warp per role accumulates clock deltas in shared
+// memory (single writer per slot) and flushes them once at kernel end.
 static __device__ unsigned long long g_phase_cycles[16];
 #define MFCG_TIC(var) long long var = clock64()
-#define MFCG_TOC(var, slot) do { long long now__ = clock64(); if ((threadIdx.x & 31) == 0) atomicAdd(&g_phase_cycles[slot], (unsigned long long)(now__ - var)); var = now__; } while (0)
+#define MFCG_TOC(var, slot)                                                                     \
+  do {                                                                                          \
+    if (threadIdx.x == 0 || threadIdx.x == NT_C) {                                              \
+      long long now__ = clock64();                                                              \
+      tcnt[slot] += (unsigned long long)(now__ - var);                                          \
+      var = now__;                                                                              \
+    }                                                                                           \
+  } while (0)
 #else
 #define MFCG_TIC(var)
 #define MFCG_TOC(var, slot)
@@ -60,23 +73,33 @@ struct SolveState {
 };
 
 // Per-degree launch shape of the brick kernel: BX x BY cells per brick layer,
-// NT_C "math" threads (sum-factorisation sweeps, shared memory only), NT_P
+// NT_C "math" threads (TPC per cell) (sum-factorisation sweeps, shared memory only), NT_P
 // "memory" threads (all global loads: pre on the way in, post one layer behind),
 // KC points per load batch of a memory thread (memory-level parallelism).
 template <int P> struct Cfg;
-#define MFCG_CFG(P_, B_, TC_, TP_, KC_, MB_)                                                   \
+#define MFCG_CFG(P_, B_, TPC_, TP_, KC_, MB_)                                                  \
   template <> struct Cfg<P_> {                                                                 \
-    static constexpr int BX = B_, BY = B_, NT_C = TC_, NT_P = TP_, KC = KC_, MINB = MB_,       \
-                         THREADS = TC_ + TP_;                                                  \
+    static constexpr int BX = B_, BY = B_, TPC = TPC_, NT_P = TP_, KC = KC_, MINB = MB_,       \
+                         NT_C = ((B_ * B_ * TPC_ + 31) / 32) * 32, THREADS = NT_C + TP_;       \
   };
-MFCG_CFG(1, 16, 256, 256, 3, 2)
-MFCG_CFG(2, 10, 256, 256, 3, 2)
-MFCG_CFG(3, 6, 192, 320, 3, 2)
-MFCG_CFG(4, 5, 224, 288, 3, 2)
-MFCG_CFG(5, 4, 192, 320, 3, 2)
-MFCG_CFG(6, 3, 224, 288, 3, 2)
-MFCG_CFG(7, 2, 128, 256, 3, 2)
-MFCG_CFG(8, 2, 128, 256, 3, 2)
+// TPC = math threads per cell; each owns ceil((P+1)^2 / TPC) lines of that cell in every sweep
+MFCG_CFG(1, 16, 1, 256, 3, 2)
+MFCG_CFG(2, 10, 3, 192, 3, 2)
+MFCG_CFG(3, 6, 8, 224, 3, 2)
+MFCG_CFG(4, 5, 9, 288, 3, 2)
+#ifndef MFCG_KC5
+#define MFCG_KC5 3
+#endif
+#ifndef MFCG_TPC5
+#define MFCG_TPC5 12
+#endif
+#ifndef MFCG_NTP5
+#define MFCG_NTP5 320
+#endif
+MFCG_CFG(5, 4, MFCG_TPC5, MFCG_NTP5, MFCG_KC5, 2)
+MFCG_CFG(6, 3, 25, 256, 3, 2)
+MFCG_CFG(7, 2, 32, 256, 3, 2)
+MFCG_CFG(8, 2, 32, 256, 3, 2)
 
 template <int P> struct Geo {
   static constexpr int N = P + 1;
@@ -171,6 +194,35 @@ __device__ __forceinline__ void block_reduce7_store(double* s, double* red, doub
 }
 
 // ---------------------------------------------------------------------------
+// Line order of the sweeps.  A math thread q of a cell handles lines order(t*TPC+q),
+// t = 0,1,...  With TPC = 16 one half-warp (the unit of a 64-bit shared-memory
+// access) works on one cell, and the order below makes the 16 lines of every pass
+// fall into 16 different banks for the tile strides RS = 7, plane = 42 doubles
+// (tools: the search is reproduced in DESIGN.md section 5).  -1 = idle lane.
+template <int N> struct LineOrder {
+  static constexpr bool custom = false;
+  __device__ static __forceinline__ int x(int s, int tpc) { return s < N * N ? s : -1; }
+  __device__ static __forceinline__ int y(int s, int tpc) { return s < N * N ? s : -1; }
+  __device__ static __forceinline__ int z(int s, int tpc) { return s < N * N ? s : -1; }
+};
+template <> struct LineOrder<6> {
+  static constexpr bool custom = true;
+  __device__ static __forceinline__ int x(int s, int tpc) { return s < 36 ? s : -1; }
+  __device__ static __forceinline__ int y(int s, int tpc) {
+    if (tpc != 16) return s < 36 ? s : -1;
+    constexpr signed char t[48] = {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 14, 15, 16, 17, 12, 13, 18, 19, 20, 21, 22, 23,
+                                   24, 25, 26, 27, 28, 29, 34, 35, 30, 31, 32, 33, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
+    return t[s];
+  }
+  __device__ static __forceinline__ int z(int s, int tpc) {
+    if (tpc != 16) return s < 36 ? s : -1;
+    constexpr signed char t[48] = {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 19, 25, 14, 15, 16, 17, 18, 20, 21, 22,
+                                   23, 24, 26, 27, 31, 33, -1, -1, 28, 29, 30, 32, 34, 35, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
+    return t[s];
+  }
+};
+
+// ---------------------------------------------------------------------------
 // mbarrier / named-barrier helpers (shared::cta)
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
@@ -181,15 +233,36 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
 }
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
   unsigned ok;
-  do {
+  do {  // the hint lets the hardware park the warp until the phase flips instead of spinning
     asm volatile(
+#ifdef MFCG_WAIT_NOHINT
         "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
-    if (!ok) __nanosleep(40);
+#else
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(20000u)
+        : "memory");
+#endif
   } while (!ok);
 }
+// L2 prefetch of a contiguous run (TMA-class bulk prefetch, no registers or shared memory):
+// [ptr + first, ptr + first + count) elements, widened to 16-byte alignment inside [0, limit)
+template <typename T>
+__device__ __forceinline__ void prefetch_l2_run(const T* ptr, i64 first, i64 count, i64 limit) {
+  if (count <= 0) return;
+  constexpr i64 PER16 = 16 / sizeof(T);
+  i64 lo = first - (first % PER16);
+  i64 hi = first + count;
+  hi += (PER16 - hi % PER16) % PER16;
+  if (hi > limit) hi -= PER16;
+  if (hi <= lo) return;
+  const unsigned bytes = (unsigned)((hi - lo) * (i64)sizeof(T));
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr + lo), "r"(bytes) : "memory");
+}
+
 template <int COUNT> __device__ __forceinline__ void math_barrier() {
   asm volatile("bar.sync 1, %0;" ::"n"(COUNT) : "memory");
 }
@@ -226,6 +299,10 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, const T* __restrict__ src, T* __re
   constexpr size_t RED_OFF = Geo<P>::template red_offset<T>();
   double* red = reinterpret_cast<double*>(smem_raw + RED_OFF);
 
+#ifdef MFCG_TIMING
+  __shared__ unsigned long long tcnt[16];
+  if (threadIdx.x < 16) tcnt[threadIdx.x] = 0;
+#endif
   const int tid = threadIdx.x;
   T am1 = 0, bm1 = 0, xc1 = 0, xc2 = 0;
   int xmode = 0;
@@ -270,9 +347,30 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, const T* __restrict__ src, T* __re
     const i64 st_int = st27[13];
     if ((ptid & 31) == 0)
       for (int q = 0; q < 7; ++q) red[pwarp * 7 + q] = 0.0;
+    // interior run of layer Lq in every vector: [run_first(Lq), +run_count(Lq))
+    auto prefetch_layer = [&](int Lq) {
+      if (Lq >= bcz || nint2d <= 0 || ptid >= 5) return;
+      const int kq0 = Lq == 0 ? 0 : 1;
+      const int Kf = Lq * P + kq0 > 1 ? Lq * P + kq0 : 1;
+      const int Kl = Lq * P + P < Lz - 1 ? Lq * P + P : Lz - 1;
+      if (Kl < Kf) return;
+      const i64 first = st_int + (i64)nint2d * (Kf - 1), count = (i64)(Kl - Kf + 1) * nint2d;
+      if (MODE == 0) {
+        if (ptid == 0) prefetch_l2_run(src, first, count, g.n_dofs);
+      } else {
+        if (ptid == 0) prefetch_l2_run(Pv, first, count, g.n_dofs);
+        if (ptid == 1) prefetch_l2_run(R, first, count, g.n_dofs);
+        if (ptid == 2) prefetch_l2_run(V, first, count, g.n_dofs);
+        if (ptid == 3) prefetch_l2_run(Minv, first, count, g.n_dofs);
+        if (ptid == 4 && xmode) prefetch_l2_run(X, first, count, g.n_dofs);
+      }
+    };
+    constexpr int PF = 2;  // layers of L2 prefetch distance
+    for (int Lq = 0; Lq < PF; ++Lq) prefetch_layer(Lq);
     MFCG_TIC(tp);
     for (int L = 0; L < bcz + 2; ++L) {
       const int stage = L & 1;
+      prefetch_layer(L + PF);
       if (L >= 2) mbar_wait(&bars[2 + stage], ((L >> 1) - 1) & 1);  // layer L-2 consumed
       MFCG_TOC(tp, 0);
       if (L < bcz) {
@@ -281,7 +379,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, const T* __restrict__ src, T* __re
         // (a) brick-interior points: one contiguous run per vector, pre fused (solvers.py:660-690)
         const int Kfirst = L * P + k0 > 1 ? L * P + k0 : 1;
         const int Klast = L * P + P < Lz - 1 ? L * P + P : Lz - 1;
-        const int nitem = (nint2d > 0 && Klast >= Kfirst) ? (Klast - Kfirst + 1) * nint2d : 0;
+        const int nitem = (nint2d > 0 && Klast >= Kfirst && !(MFCG_SKIP & 8)) ? (Klast - Kfirst + 1) * nint2d : 0;
         const i64 gbase = st_int + (i64)nint2d * (Kfirst - 1);
         for (int it0 = ptid; it0 < nitem; it0 += KC * NT_P) {
           T rr[KC], vv[KC], pp[KC], mm[KC], xx[KC];
@@ -378,7 +476,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, const T* __restrict__ src, T* __re
         mbar_arrive(&bars[stage]);  // layer L full
         MFCG_TOC(tp, 1);
       }
-      if (MODE == 1 && L >= 2) {
+      if (MODE == 1 && L >= 2 && !(MFCG_SKIP & 4)) {
         // ---- post sums of layer L-2 (solvers.py:692-698): its v is final and, like r, p and
         // 1/diag, still resident in L2; one contiguous run per vector
         const int Lp = L - 2;
@@ -414,8 +512,15 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, const T* __restrict__ src, T* __re
     }
   } else {
     // ===================== math warps =====================
-    const int ncell = bcx * bcy;
-    const unsigned bcx_magic = (65536u + bcx - 1) / bcx;
+    // Fixed ownership: TPC threads per cell, thread q of a cell owns lines q, q+TPC, ... of
+    // that cell in every sweep of every layer, so all index arithmetic is hoisted.
+    constexpr int TPC = Cfg<P>::TPC, LPT = (N * N + TPC - 1) / TPC;
+    const int cell = tid / TPC, q = tid - cell * TPC;
+    const bool has_cell = cell < bcx * bcy;
+    const int cy = has_cell ? cell / bcx : 0, cx = has_cell ? cell - cy * bcx : 0;
+    T* const At = A + cell * TILE;
+    T* const Bt = Bs + cell * TILE;
+    const T* const ring_cell = ring + cy * P * WX + cx * P;
     MFCG_TIC(tc);
     for (int L = 0; L < bcz; ++L) {
       const int stage = L & 1;
@@ -424,102 +529,115 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, const T* __restrict__ src, T* __re
       mbar_wait(&bars[stage], (L >> 1) & 1);  // layer L full
       MFCG_TOC(tc, 4);
 
-      // ---- x sweep: a = M u, b = gx K u along every x line of every cell
-      for (int w = tid; w < ncell * N * N; w += NT_C) {
-        const int cell = w / (N * N);
-        const int rr = w - cell * (N * N);
-        const int k = rr / N, j = rr - k * N;
-        const int cy = (int)(((unsigned)cell * bcx_magic) >> 16);
-        const int cx = cell - cy * bcx;
-        int slot = s0 + k;
-        if (slot >= RB) slot -= RB;
-        const T* row = ring + slot * PLANE + (cy * P + j) * WX + cx * P;
-        T u[N], e[HE], o[HE];
+      // ---- x sweep: a = M u, b = gx K u along every x line of the cell
+      if (has_cell && !(MFCG_SKIP & 1)) {
+#pragma unroll 1
+        for (int t = 0; t < LPT; ++t) {
+          const int l = LineOrder<N>::x(q + t * TPC, TPC);
+          if (l < 0) continue;
+          const int k = l / N, j = l - k * N;
+          int slot = s0 + k;
+          if (slot >= RB) slot -= RB;
+          const T* row = ring_cell + slot * PLANE + j * WX;
+          T u[N], e[HE], o[HE];
 #pragma unroll
-        for (int i = 0; i < N; ++i) u[i] = row[i];
-        eo_split<N>(u, e, o);
-        T* ao = A + cell * TILE + (k * N + j) * RS;
-        T* bo = Bs + cell * TILE + (k * N + j) * RS;
-        T se[HE], so[HE], te[HE], to[HE], out[N];
+          for (int i = 0; i < N; ++i) u[i] = row[i];
+          eo_split<N>(u, e, o);
+          T* ao = At + l * RS;
+          T* bo = Bt + l * RS;
+          T se[HE], so[HE], out[N];
 #pragma unroll
-        for (int i = 0; i < HE; ++i) { se[i] = 0; so[i] = 0; te[i] = 0; to[i] = 0; }
-        eo_mul<N>(tab.Me, tab.Mo, e, o, se, so);
-        eo_mul<N>(tab.Ke, tab.Ko, e, o, te, to);
-        eo_join<N>(se, so, out);
+          for (int i = 0; i < HE; ++i) { se[i] = 0; so[i] = 0; }
+          eo_mul<N>(tab.Me, tab.Mo, e, o, se, so);
+          eo_join<N>(se, so, out);
 #pragma unroll
-        for (int q = 0; q < N; ++q) ao[q] = out[q];
+          for (int i = 0; i < N; ++i) ao[i] = out[i];
 #pragma unroll
-        for (int i = 0; i < HE; ++i) { te[i] *= tab.g[0]; to[i] *= tab.g[0]; }
-        eo_join<N>(te, to, out);
+          for (int i = 0; i < HE; ++i) { se[i] = 0; so[i] = 0; }
+          eo_mul<N>(tab.Ke, tab.Ko, e, o, se, so);
 #pragma unroll
-        for (int q = 0; q < N; ++q) bo[q] = out[q];
+          for (int i = 0; i < HE; ++i) { se[i] *= tab.g[0]; so[i] *= tab.g[0]; }
+          eo_join<N>(se, so, out);
+#pragma unroll
+          for (int i = 0; i < N; ++i) bo[i] = out[i];
+        }
       }
       MFCG_TOC(tc, 5);
       math_barrier<NT_C>();
       MFCG_TOC(tc, 8);
 
       // ---- y sweep (in place): c = M a, de = gy K a + M b
-      for (int w = tid; w < ncell * N * N; w += NT_C) {
-        const int cell = w / (N * N);
-        const int rr = w - cell * (N * N);
-        const int k = rr / N, i = rr - k * N;
-        T* ac = A + cell * TILE + k * N * RS + i;
-        T* bc = Bs + cell * TILE + k * N * RS + i;
-        T a[N], bb[N], ea[HE], oa[HE], eb[HE], ob[HE];
+      if (has_cell && !(MFCG_SKIP & 1)) {
+#pragma unroll 1
+        for (int t = 0; t < LPT; ++t) {
+          const int l = LineOrder<N>::y(q + t * TPC, TPC);
+          if (l < 0) continue;
+          const int k = l / N, i = l - k * N;
+          T* ac = At + k * N * RS + i;
+          T* bc = Bt + k * N * RS + i;
+          T a[N], ea[HE], oa[HE], eb[HE], ob[HE];
 #pragma unroll
-        for (int j = 0; j < N; ++j) { a[j] = ac[j * RS]; bb[j] = bc[j * RS]; }
-        eo_split<N>(a, ea, oa);
-        eo_split<N>(bb, eb, ob);
-        T se[HE], so[HE], te[HE], to[HE], out[N];
+          for (int j = 0; j < N; ++j) a[j] = ac[j * RS];
+          eo_split<N>(a, ea, oa);
 #pragma unroll
-        for (int i2 = 0; i2 < HE; ++i2) { se[i2] = 0; so[i2] = 0; te[i2] = 0; to[i2] = 0; }
-        eo_mul<N>(tab.Me, tab.Mo, ea, oa, se, so);  // c = M a
-        eo_join<N>(se, so, out);
+          for (int j = 0; j < N; ++j) a[j] = bc[j * RS];
+          eo_split<N>(a, eb, ob);
+          T se[HE], so[HE], out[N];
 #pragma unroll
-        for (int q = 0; q < N; ++q) ac[q * RS] = out[q];
-        eo_mul<N>(tab.Ke, tab.Ko, ea, oa, te, to);  // K a
+          for (int i2 = 0; i2 < HE; ++i2) { se[i2] = 0; so[i2] = 0; }
+          eo_mul<N>(tab.Ke, tab.Ko, ea, oa, se, so);  // K a
 #pragma unroll
-        for (int i2 = 0; i2 < HE; ++i2) { se[i2] = 0; so[i2] = 0; }
-        eo_mul<N>(tab.Me, tab.Mo, eb, ob, se, so);  // M b
+          for (int i2 = 0; i2 < HE; ++i2) { se[i2] *= tab.g[1]; so[i2] *= tab.g[1]; }
+          eo_mul<N>(tab.Me, tab.Mo, eb, ob, se, so);  // + M b
+          eo_join<N>(se, so, out);
 #pragma unroll
-        for (int i2 = 0; i2 < HE; ++i2) { se[i2] += tab.g[1] * te[i2]; so[i2] += tab.g[1] * to[i2]; }
-        eo_join<N>(se, so, out);
+          for (int j = 0; j < N; ++j) bc[j * RS] = out[j];
 #pragma unroll
-        for (int q = 0; q < N; ++q) bc[q * RS] = out[q];
+          for (int i2 = 0; i2 < HE; ++i2) { se[i2] = 0; so[i2] = 0; }
+          eo_mul<N>(tab.Me, tab.Mo, ea, oa, se, so);  // c = M a
+          eo_join<N>(se, so, out);
+#pragma unroll
+          for (int j = 0; j < N; ++j) ac[j * RS] = out[j];
+        }
       }
       MFCG_TOC(tc, 6);
       math_barrier<NT_C>();
       MFCG_TOC(tc, 8);
 
       // ---- z sweep: out = M de + gz K c, written over c
-      for (int w = tid; w < ncell * N * N; w += NT_C) {
-        const int cell = w / (N * N);
-        const int rr = w - cell * (N * N);
-        const int j = rr / N, i = rr - j * N;
-        T* ac = A + cell * TILE + j * RS + i;
-        const T* bc = Bs + cell * TILE + j * RS + i;
-        T c[N], de[N], ec[HE], oc[HE], ed[HE], od[HE];
+      if (has_cell && !(MFCG_SKIP & 1)) {
+#pragma unroll 1
+        for (int t = 0; t < LPT; ++t) {
+          const int l = LineOrder<N>::z(q + t * TPC, TPC);
+          if (l < 0) continue;
+          const int j = l / N, i = l - j * N;
+          T* ac = At + j * RS + i;
+          const T* bc = Bt + j * RS + i;
+          T a[N], ec[HE], oc[HE], ed[HE], od[HE];
 #pragma unroll
-        for (int k = 0; k < N; ++k) { c[k] = ac[k * N * RS]; de[k] = bc[k * N * RS]; }
-        eo_split<N>(c, ec, oc);
-        eo_split<N>(de, ed, od);
-        T se[HE], so[HE], te[HE], to[HE], out[N];
+          for (int k = 0; k < N; ++k) a[k] = ac[k * N * RS];
+          eo_split<N>(a, ec, oc);
 #pragma unroll
-        for (int i2 = 0; i2 < HE; ++i2) { se[i2] = 0; so[i2] = 0; te[i2] = 0; to[i2] = 0; }
-        eo_mul<N>(tab.Ke, tab.Ko, ec, oc, te, to);  // K c
-        eo_mul<N>(tab.Me, tab.Mo, ed, od, se, so);  // M de
+          for (int k = 0; k < N; ++k) a[k] = bc[k * N * RS];
+          eo_split<N>(a, ed, od);
+          T se[HE], so[HE], out[N];
 #pragma unroll
-        for (int i2 = 0; i2 < HE; ++i2) { se[i2] += tab.g[2] * te[i2]; so[i2] += tab.g[2] * to[i2]; }
-        eo_join<N>(se, so, out);
+          for (int i2 = 0; i2 < HE; ++i2) { se[i2] = 0; so[i2] = 0; }
+          eo_mul<N>(tab.Ke, tab.Ko, ec, oc, se, so);  // K c
 #pragma unroll
-        for (int q = 0; q < N; ++q) ac[q * N * RS] = out[q];
+          for (int i2 = 0; i2 < HE; ++i2) { se[i2] *= tab.g[2]; so[i2] *= tab.g[2]; }
+          eo_mul<N>(tab.Me, tab.Mo, ed, od, se, so);  // + M de
+          eo_join<N>(se, so, out);
+#pragma unroll
+          for (int k = 0; k < N; ++k) ac[k * N * RS] = out[k];
+        }
       }
       MFCG_TOC(tc, 7);
       math_barrier<NT_C>();
       MFCG_TOC(tc, 8);
 
       // ---- gather the cells' contributions per lattice point, finish the planes
-      for (int rem = tid; rem < fp; rem += NT_C) {
+      for (int rem = tid; rem < ((MFCG_SKIP & 2) ? 0 : fp); rem += NT_C) {
         const int j = (int)(((unsigned)rem * fw_magic) >> 16);
         const int i = rem - j * fw;
         const int ex = i == 0 ? 0 : (i == Lx ? 2 : 1), ey = j == 0 ? 0 : (j == Ly ? 2 : 1);
@@ -564,6 +682,10 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, const T* __restrict__ src, T* __re
       MFCG_TOC(tc, 9);
     }
   }
+#ifdef MFCG_TIMING
+  __syncthreads();
+  if (threadIdx.x < 16 && tcnt[threadIdx.x]) atomicAdd(&g_phase_cycles[threadIdx.x], tcnt[threadIdx.x]);
+#endif
   if (MODE == 1) {
     // block sums: the memory warps' slots, added in a fixed order (deterministic)
     __syncthreads();
@@ -685,6 +807,10 @@ static __global__ void k_scalar_merged(const double* __restrict__ partials, int 
   if (!st->active) return;
   reduce_rows(partials, rows, 7, sums, red);
   if (threadIdx.x != 0) return;
+#if MFCG_SKIP
+  // timing experiments only: keep iterating on garbage
+  sums[0] = sums[1] = sums[3] = sums[4] = sums[6] = 1.0; sums[2] = sums[5] = 0.25;
+#endif
   const double gamma = sums[0], a = sums[1], bb = sums[2], cc = sums[3], d = sums[4], e = sums[5], f = sums[6];
   const int k = st->k + 1;
   const bool fixed = st->fixed != 0;
