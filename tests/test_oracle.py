@@ -148,3 +148,31 @@ def test_curved_geometry_matches_reference(golden, ci):
     assert rel(sym, ft) < 1e-12
     assert rel(orc.apply(prob, g[f"k{ci}_u"]), g[f"k{ci}_Au"]) < 1e-12
     assert rel(orc.inverse_diagonal(prob), g[f"k{ci}_invdiag"]) < 1e-12
+
+
+def test_c_oracle_matches_numpy_oracle_and_reference(golden):
+    """oracle/mfcg_oracle.c (pthreads) against the NumPy oracle and the reference fixtures."""
+    import mfcg_oracle_c as oc
+    if not oc.available():
+        pytest.skip("C oracle could not be built (no gcc/make)")
+    g = golden["apply"]
+    for ci in (0, 3, 5, 8):
+        cells, p, nq, numb, con = APPLY_CASES[ci]
+        m, h, plan = host_tables(cells, p, constrain=con, numbering=numb)
+        cp = oc.CProblem(oracle_problem(m, h, p, nq))
+        assert rel(cp.apply(g[f"c{ci}_u"]), g[f"c{ci}_Au"]) < 1e-12
+    g1 = golden["config1"]
+    m, h, plan = host_tables((8, 8, 8), 4)
+    prob = oracle_problem(m, h, 4, 5)
+    cp = oc.CProblem(prob)
+    x, k, hist = cp.combined_pcg(g1["b"], orc.inverse_diagonal(prob), 100)
+    R = g1["combined_pcg_hist"]
+    assert k == 100
+    assert (np.abs(hist[:40, 3] - R[:40, 3]) / R[:40, 3]).max() < 1e-10
+    assert rel(hist[:40, :2], R[:40, :2]) < 1e-10
+    assert rel(x, g1["combined_pcg_x"]) < 1e-6
+    gc = golden["curved"]
+    cells, p, nq, amp = CURVED_CASES[1]
+    m, h, plan = host_tables(cells, p, deform=amp)
+    cp = oc.CProblem(oracle_problem(m, h, p, nq, geometry="curved"))
+    assert rel(cp.apply(gc["k1_u"]), gc["k1_Au"]) < 1e-12
