@@ -11,32 +11,34 @@ namespace mfcg {
 static thread_local std::string g_error;
 void set_error(const std::string& msg) { g_error = msg; }
 
-EngineBase* make_engine_p1(OpCommon*);
-EngineBase* make_engine_p2(OpCommon*);
-EngineBase* make_engine_p3(OpCommon*);
-EngineBase* make_engine_p4(OpCommon*);
-EngineBase* make_engine_p5(OpCommon*);
-EngineBase* make_engine_p6(OpCommon*);
-EngineBase* make_engine_p7(OpCommon*);
-EngineBase* make_engine_p8(OpCommon*);
+EngineBase* make_engine_p1(OpCommon*, int*);
+EngineBase* make_engine_p2(OpCommon*, int*);
+EngineBase* make_engine_p3(OpCommon*, int*);
+EngineBase* make_engine_p4(OpCommon*, int*);
+EngineBase* make_engine_p5(OpCommon*, int*);
+EngineBase* make_engine_p6(OpCommon*, int*);
+EngineBase* make_engine_p7(OpCommon*, int*);
+EngineBase* make_engine_p8(OpCommon*, int*);
 
-EngineBase* make_engine(OpCommon* c) {
+EngineBase* make_engine(OpCommon* c, int* status) {
   switch (c->p) {
-    case 1: return make_engine_p1(c);
-    case 2: return make_engine_p2(c);
-    case 3: return make_engine_p3(c);
-    case 4: return make_engine_p4(c);
-    case 5: return make_engine_p5(c);
-    case 6: return make_engine_p6(c);
-    case 7: return make_engine_p7(c);
-    case 8: return make_engine_p8(c);
+    case 1: return make_engine_p1(c, status);
+    case 2: return make_engine_p2(c, status);
+    case 3: return make_engine_p3(c, status);
+    case 4: return make_engine_p4(c, status);
+    case 5: return make_engine_p5(c, status);
+    case 6: return make_engine_p6(c, status);
+    case 7: return make_engine_p7(c, status);
+    case 8: return make_engine_p8(c, status);
   }
   set_error("degree must be in 1..8");
+  *status = MFCG_EINVAL;
   return nullptr;
 }
 
-// default brick extent in x and y per degree == Cfg<P>::BX (mfcg_kernels.cuh)
-static const int kBrickXY[9] = {0, 16, 10, 6, 5, 4, 3, 2, 2};
+// default brick extent in x / y per geometry class and degree == Cfg<P, G>::BX / BY (mfcg_kernels.cuh)
+static const int kBrickX[2][9] = {{0, 16, 10, 6, 5, 4, 3, 2, 2}, {0, 16, 10, 6, 5, 4, 3, 2, 2}};
+static const int kBrickY[2][9] = {{0, 16, 10, 6, 5, 4, 3, 2, 2}, {0, 16, 10, 6, 5, 3, 2, 2, 2}};
 
 }  // namespace mfcg
 
@@ -126,10 +128,7 @@ static int op_create_impl(mfcg_ctx* ctx, const mfcg_op_desc* d, mfcg_op* op) {
     set_error("affine geometry requires an undeformed mesh");  // mesh.py:214-216
     return MFCG_EINVAL;
   }
-  if (d->geometry != MFCG_GEOM_AFFINE) {
-    set_error("curved geometry variants are not built yet in this round");
-    return MFCG_EUNSUPPORTED;
-  }
+  if (d->geometry < 0 || d->geometry > 3) { set_error("unknown geometry variant"); return MFCG_EINVAL; }
   if (d->precision != 0 && d->precision != 1) { set_error("precision must be 0 (fp64) or 1 (fp32)"); return MFCG_EINVAL; }
   const i64 NX = (i64)d->cells[0] * p + 1, NY = (i64)d->cells[1] * p + 1, NZ = (i64)d->cells[2] * p + 1;
   if (d->n_dofs != NX * NY * NZ) {
@@ -160,8 +159,10 @@ static int op_create_impl(mfcg_ctx* ctx, const mfcg_op_desc* d, mfcg_op* op) {
   }
   // brick extents: x, y bounded by the kernel's shared-memory window; z free
   for (int k = 0; k < 2; ++k) {
-    int b = d->brick[k] > 0 ? d->brick[k] : kBrickXY[p];
-    if (b > kBrickXY[p]) { set_error("brick extent in x/y exceeds the kernel window for this degree"); return MFCG_EINVAL; }
+    const int gclass = d->geometry == MFCG_GEOM_AFFINE ? 0 : 1;
+    const int cap = k == 0 ? kBrickX[gclass][p] : kBrickY[gclass][p];
+    int b = d->brick[k] > 0 ? d->brick[k] : cap;
+    if (b > cap) { set_error("brick extent in x/y exceeds the kernel window for this degree"); return MFCG_EINVAL; }
     g.B[k] = std::min(b, g.cells[k]);
   }
   {
@@ -256,8 +257,9 @@ static int op_create_impl(mfcg_ctx* ctx, const mfcg_op_desc* d, mfcg_op* op) {
       return MFCG_EUNSUPPORTED;
     }
   }
-  op->engine = make_engine(&c);
-  if (!op->engine) return MFCG_ECUDA;
+  int est = MFCG_ECUDA;
+  op->engine = make_engine(&c, &est);
+  if (!op->engine) return est == MFCG_OK ? MFCG_ECUDA : est;
   MFCG_CUDA(cudaStreamSynchronize(st));
   return MFCG_OK;
 }
@@ -304,9 +306,9 @@ int mfcg_op_diagonal(mfcg_op* op, double* inv_diag, int location) {
 }
 
 int mfcg_op_geometry(mfcg_op* op, int kind, double* out_host, int64_t n_doubles) {
-  (void)op; (void)kind; (void)out_host; (void)n_doubles;
-  set_error("curved geometry variants are not built yet in this round");
-  return MFCG_EUNSUPPORTED;
+  if (!op || !out_host) { set_error("NULL argument"); return MFCG_EINVAL; }
+  cudaSetDevice(op->common.ctx->device);
+  return op->engine->geometry(kind, out_host, n_doubles);
 }
 
 int mfcg_solve(mfcg_op* op, const mfcg_solve_args* args, mfcg_solve_result* result) {

@@ -1,6 +1,7 @@
 // mfcg_engine.cuh -- host-side engine: owns device memory, launches the kernels,
 // runs the device-resident CG loops.  One Engine<P, T> per (degree, precision).
 #pragma once
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -56,6 +57,7 @@ struct EngineBase {
   virtual int diagonal(double* out, int location) = 0;
   virtual int solve(const mfcg_solve_args* a, mfcg_solve_result* r) = 0;
   virtual void info(mfcg_op_info* out) = 0;
+  virtual int geometry(int kind, double* out_host, i64 n_doubles) = 0;
 };
 
 template <int P, typename T>
@@ -71,6 +73,8 @@ class Engine : public EngineBase {
     if (partials_a_) cudaFree(partials_a_);
     if (partials_b_) cudaFree(partials_b_);
     if (d_history_) cudaFree(d_history_);
+    if (geo_a_) cudaFree(geo_a_);
+    if (geo_b_) cudaFree(geo_b_);
     for (cudaEvent_t e : events_) cudaEventDestroy(e);
   }
 
@@ -112,10 +116,22 @@ class Engine : public EngineBase {
     pack(M, tab_.Me, tab_.Mo);
     pack(K, tab_.Ke, tab_.Ko);
     for (int d = 0; d < 3; ++d) tab_.g[d] = (T)(det / (c_->h[d] * c_->h[d]));
-    // the mass factor of the cell volume is carried by the K's: A_e = sum_d Kd (x) M (x) M
-    smem_ = (int)Geo<P>::template smem_bytes<T>();
-    MFCG_CUDA(cudaFuncSetAttribute(k_brick<P, T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
-    MFCG_CUDA(cudaFuncSetAttribute(k_brick<P, T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
+    general_ = c_->geometry != MFCG_GEOM_AFFINE;
+    if (general_) {
+      if (c_->nq != N) {
+        set_error("curved geometry variants need n_q_1d == p+1 on the GPU path");
+        return MFCG_EUNSUPPORTED;
+      }
+      smem_ = (int)Geo<P, 1>::template smem_bytes<T>();
+      MFCG_CUDA(cudaFuncSetAttribute(k_brick<P, T, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
+      MFCG_CUDA(cudaFuncSetAttribute(k_brick<P, T, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
+      int rc = build_general_tables();
+      if (rc) return rc;
+    } else {
+      smem_ = (int)Geo<P, 0>::template smem_bytes<T>();
+      MFCG_CUDA(cudaFuncSetAttribute(k_brick<P, T, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
+      MFCG_CUDA(cudaFuncSetAttribute(k_brick<P, T, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
+    }
     vgrid_ = c_->ctx->sm_count * 8;
     const i64 rows = c_->n_bricks + vgrid_;
     MFCG_CUDA(cudaMalloc(&partials_a_, sizeof(double) * 8 * rows));
@@ -130,9 +146,9 @@ class Engine : public EngineBase {
     out->n_interior = c_->grid.n_int;
     out->n_bricks = c_->n_bricks;
     for (int d = 0; d < 3; ++d) out->brick[d] = c_->grid.B[d];
-    out->threads = Cfg<P>::THREADS;
+    out->threads = general_ ? Cfg<P, 1>::THREADS : Cfg<P, 0>::THREADS;
     out->smem_bytes = smem_;
-    out->geometry_bytes = 0;
+    out->geometry_bytes = geo_bytes_;
   }
 
   int apply(const double* src, double* dst, int location) override {
@@ -159,6 +175,26 @@ class Engine : public EngineBase {
 
   int solve(const mfcg_solve_args* a, mfcg_solve_result* res) override;
 
+  // copies the device-built table back as fp64: kind 1 final tensor, kind 2 inverse Jacobian then jxw
+  int geometry(int kind, double* out_host, i64 n_doubles) override {
+    if (!general_ || kind != c_->geometry || (kind != 1 && kind != 2)) {
+      set_error("the operator holds no stored geometry table of that kind");
+      return MFCG_EINVAL;
+    }
+    const i64 nq3 = (i64)N * N * N, nc = c_->n_cells;
+    const i64 need = kind == 1 ? nc * nq3 * 6 : nc * nq3 * 10;
+    if (n_doubles < need) { set_error("output buffer too small"); return MFCG_EINVAL; }
+    const i64 na = kind == 1 ? nc * nq3 * 6 : nc * nq3 * 9;
+    std::vector<T> tmp((size_t)std::max(na, nc * nq3));
+    MFCG_CUDA(cudaMemcpy(tmp.data(), geo_a_, sizeof(T) * na, cudaMemcpyDeviceToHost));
+    for (i64 i = 0; i < na; ++i) out_host[i] = (double)tmp[(size_t)i];
+    if (kind == 2) {
+      MFCG_CUDA(cudaMemcpy(tmp.data(), geo_b_, sizeof(T) * nc * nq3, cudaMemcpyDeviceToHost));
+      for (i64 i = 0; i < nc * nq3; ++i) out_host[na + i] = (double)tmp[(size_t)i];
+    }
+    return MFCG_OK;
+  }
+
  private:
   cudaStream_t stream() const { return c_->ctx->stream; }
 
@@ -173,25 +209,40 @@ class Engine : public EngineBase {
 
   int ensure_diagonal() {
     if (c_->d_invdiag) return MFCG_OK;
-    if (c_->geometry != MFCG_GEOM_AFFINE) {
-      set_error("Jacobi diagonal on curved geometry is not built yet in this round");
-      return MFCG_EUNSUPPORTED;
-    }
     const i64 n = c_->grid.n_dofs;
     double* diag = nullptr;
     MFCG_CUDA(cudaMalloc(&diag, sizeof(double) * n));
     MFCG_CUDA(cudaMemsetAsync(diag, 0, sizeof(double) * n, stream()));
-    DiagTables t{};
-    for (int i = 0; i < N; ++i) {
-      t.w[i] = c_->glw[i];
-      double dd = 0.0;
-      for (int q = 0; q < N; ++q) dd += c_->glw[q] * c_->glD[q * N + i] * c_->glD[q * N + i];
-      t.dd[i] = dd;
+    MFCG_CUDA(cudaMemsetAsync(c_->d_flag, 0, sizeof(int), stream()));
+    if (!general_) {
+      DiagTables t{};
+      for (int i = 0; i < N; ++i) {
+        t.w[i] = c_->glw[i];
+        double dd = 0.0;
+        for (int q = 0; q < N; ++q) dd += c_->glw[q] * c_->glD[q * N + i] * c_->glD[q * N + i];
+        t.dd[i] = dd;
+      }
+      const double det = c_->h[0] * c_->h[1] * c_->h[2];
+      for (int d = 0; d < 3; ++d) t.g[d] = det / (c_->h[d] * c_->h[d]);
+      k_diag_affine<<<vgrid_, VT, 0, stream()>>>(c_->grid, t, c_->n_cells, diag);
+    } else {
+      DiagGen dg{};
+      for (int q = 0; q < N; ++q)
+        for (int i = 0; i < N; ++i) dg.D2[q * N + i] = c_->glD[q * N + i] * c_->glD[q * N + i];
+      for (int i = 0; i < N; ++i) dg.dd[i] = c_->glD[i * N + i];
+      const PointTab pt = point_table(c_->glx, c_->glw);
+      const size_t sm = sizeof(double) * 6 * N * N * N;
+      k_diag_general<<<vgrid_, 128, sm, stream()>>>(c_->grid, geo_mesh(), pt, dg, c_->n_cells, diag, c_->d_flag);
     }
-    const double det = c_->h[0] * c_->h[1] * c_->h[2];
-    for (int d = 0; d < 3; ++d) t.g[d] = det / (c_->h[d] * c_->h[d]);
-    k_diag_affine<<<vgrid_, VT, 0, stream()>>>(c_->grid, t, c_->n_cells, diag);
     MFCG_CUDA(cudaGetLastError());
+    int gflag = 0;
+    MFCG_CUDA(cudaMemcpyAsync(&gflag, c_->d_flag, sizeof(int), cudaMemcpyDeviceToHost, stream()));
+    MFCG_CUDA(cudaStreamSynchronize(stream()));
+    if (gflag) {
+      cudaFree(diag);
+      set_error("degenerate cell: det J <= 0");
+      return MFCG_EINVAL;
+    }
     MFCG_CUDA(cudaMemsetAsync(c_->d_flag, 0, sizeof(int), stream()));
     k_diag_invert<<<vgrid_, VT, 0, stream()>>>(c_->grid, diag, c_->d_flag);
     MFCG_CUDA(cudaGetLastError());
@@ -244,12 +295,22 @@ class Engine : public EngineBase {
       e1 = events_[event_cursor_++];
       MFCG_CUDA(cudaEventRecord(e0, stream()));
     }
-    if (mode == 0)
-      k_brick<P, T, 0><<<(unsigned)c_->n_bricks, Cfg<P>::THREADS, smem_, stream()>>>(
-          c_->grid, tab_, src, nullptr, v, nullptr, nullptr, nullptr, nullptr, nullptr);
-    else
-      k_brick<P, T, 1><<<(unsigned)c_->n_bricks, Cfg<P>::THREADS, smem_, stream()>>>(
-          c_->grid, tab_, nullptr, pv, v, r_, x_, minv_, c_->d_state, partials);
+    const unsigned nb = (unsigned)c_->n_bricks;
+    if (!general_) {
+      if (mode == 0)
+        k_brick<P, T, 0, 0><<<nb, Cfg<P, 0>::THREADS, smem_, stream()>>>(
+            c_->grid, tab_, gen_, geo_, src, nullptr, v, nullptr, nullptr, nullptr, nullptr, nullptr);
+      else
+        k_brick<P, T, 1, 0><<<nb, Cfg<P, 0>::THREADS, smem_, stream()>>>(
+            c_->grid, tab_, gen_, geo_, nullptr, pv, v, r_, x_, minv_, c_->d_state, partials);
+    } else {
+      if (mode == 0)
+        k_brick<P, T, 0, 1><<<nb, Cfg<P, 1>::THREADS, smem_, stream()>>>(
+            c_->grid, tab_, gen_, geo_, src, nullptr, v, nullptr, nullptr, nullptr, nullptr, nullptr);
+      else
+        k_brick<P, T, 1, 1><<<nb, Cfg<P, 1>::THREADS, smem_, stream()>>>(
+            c_->grid, tab_, gen_, geo_, nullptr, pv, v, r_, x_, minv_, c_->d_state, partials);
+    }
     MFCG_CUDA(cudaGetLastError());
     if (time_kernels_) MFCG_CUDA(cudaEventRecord(e1, stream()));
     ++launches_;
@@ -275,11 +336,107 @@ class Engine : public EngineBase {
     return MFCG_OK;
   }
 
+  GeoMesh geo_mesh() const {
+    GeoMesh gm{};
+    for (int d = 0; d < 3; ++d) { gm.cells[d] = c_->grid.cells[d]; gm.h[d] = c_->h[d]; gm.ext[d] = c_->extents[d]; }
+    gm.amp = c_->deformation;
+    return gm;
+  }
+
+  // quadratic Lagrange basis on {0, 1/2, 1} and its derivative at 1D points t (mesh.py:150-170)
+  static PointTab point_table(const std::vector<double>& t, const std::vector<double>& w) {
+    PointTab pt{};
+    pt.n = (int)t.size();
+    for (int i = 0; i < pt.n; ++i) {
+      const double x = t[i];
+      pt.qv[3 * i + 0] = 2.0 * (x - 0.5) * (x - 1.0); pt.qv[3 * i + 1] = -4.0 * x * (x - 1.0); pt.qv[3 * i + 2] = 2.0 * x * (x - 0.5);
+      pt.qd[3 * i + 0] = 4.0 * x - 3.0; pt.qd[3 * i + 1] = 4.0 - 8.0 * x; pt.qd[3 * i + 2] = 4.0 * x - 1.0;
+      pt.w[i] = w[i];
+    }
+    return pt;
+  }
+
+  // halves of S and of the collocation derivative Dc, and the device geometry tables
+  int build_general_tables() {
+    constexpr int H = EOShape<N>::H, HE = EOShape<N>::HE;
+    const std::vector<double>& S = c_->S;  // [q][i], n_q == N
+    // Dc[q][r]: derivative at x_q of the Lagrange polynomial through the quadrature points
+    std::vector<double> Dc(N * N, 0.0);
+    const std::vector<double>& x = c_->xq;
+    for (int r = 0; r < N; ++r) {
+      double wr = 1.0;
+      for (int j = 0; j < N; ++j) if (j != r) wr /= (x[r] - x[j]);
+      for (int q = 0; q < N; ++q) {
+        double acc = 0.0;
+        for (int m = 0; m < N; ++m) {
+          if (m == r) continue;
+          double prod = 1.0;
+          for (int j = 0; j < N; ++j) if (j != r && j != m) prod *= (x[q] - x[j]);
+          acc += prod;
+        }
+        Dc[q * N + r] = wr * acc;
+      }
+    }
+    for (int q = 0; q < HE; ++q)
+      for (int i = 0; i < HE; ++i) {
+        const bool mid = (N & 1) && i == H;
+        gen_.Se[q * HE + i] = (T)(mid ? S[q * N + i] : 0.5 * (S[q * N + i] + S[q * N + (N - 1 - i)]));
+      }
+    for (int q = 0; q < H; ++q)
+      for (int i = 0; i < H; ++i) gen_.So[q * H + i] = (T)(0.5 * (S[q * N + i] - S[q * N + (N - 1 - i)]));
+    for (int q = 0; q < H; ++q)
+      for (int r = 0; r < HE; ++r) {
+        const bool mid = (N & 1) && r == H;
+        gen_.Be[q * HE + r] = (T)(mid ? Dc[q * N + r] : 0.5 * (Dc[q * N + r] + Dc[q * N + (N - 1 - r)]));
+      }
+    for (int q = 0; q < HE; ++q)
+      for (int r = 0; r < H; ++r) gen_.Bo[q * H + r] = (T)(0.5 * (Dc[q * N + r] - Dc[q * N + (N - 1 - r)]));
+    const PointTab pt = point_table(c_->xq, c_->wq);
+    for (int i = 0; i < N; ++i) {
+      for (int c = 0; c < 3; ++c) { gen_.qv[3 * i + c] = (T)pt.qv[3 * i + c]; gen_.qd[3 * i + c] = (T)pt.qd[3 * i + c]; }
+      gen_.w3[i] = (T)c_->wq[i];
+    }
+    const i64 nc = c_->n_cells, nq3 = (i64)N * N * N;
+    const int kind = c_->geometry;
+    double* nodes = nullptr;
+    MFCG_CUDA(cudaMemsetAsync(c_->d_flag, 0, sizeof(int), stream()));
+    if (kind == MFCG_GEOM_FINAL_TENSOR_LOAD) {
+      geo_bytes_ = sizeof(T) * nc * nq3 * 6;
+      MFCG_CUDA(cudaMalloc(&geo_a_, geo_bytes_));
+    } else if (kind == MFCG_GEOM_INVERSE_JACOBIAN_LOAD) {
+      geo_bytes_ = sizeof(T) * nc * nq3 * 10;
+      MFCG_CUDA(cudaMalloc(&geo_a_, sizeof(T) * nc * nq3 * 9));
+      MFCG_CUDA(cudaMalloc(&geo_b_, sizeof(T) * nc * nq3));
+    } else {
+      geo_bytes_ = sizeof(double) * nc * 81;
+      MFCG_CUDA(cudaMalloc(&geo_a_, geo_bytes_));
+      nodes = reinterpret_cast<double*>(geo_a_);
+    }
+    k_geometry<T><<<vgrid_from_ctx(), 128, 0, stream()>>>(geo_mesh(), pt, nc, kind, reinterpret_cast<T*>(geo_a_),
+                                                          reinterpret_cast<T*>(geo_b_), nodes, c_->d_flag);
+    MFCG_CUDA(cudaGetLastError());
+    int flag = 0;
+    MFCG_CUDA(cudaMemcpyAsync(&flag, c_->d_flag, sizeof(int), cudaMemcpyDeviceToHost, stream()));
+    MFCG_CUDA(cudaStreamSynchronize(stream()));
+    if (flag) { set_error("degenerate cell: det J <= 0"); return MFCG_EINVAL; }
+    geo_.kind = kind;
+    geo_.data = geo_a_;
+    geo_.jxw = geo_b_;
+    return MFCG_OK;
+  }
+  int vgrid_from_ctx() const { return c_->ctx->sm_count * 8; }
+
   int run_merged(const mfcg_solve_args* a, int limit);
   int run_standard(const mfcg_solve_args* a, int limit, bool prec);
 
   OpCommon* c_;
   SepTables<T, N> tab_{};
+  GenTables<T, N> gen_{};
+  GeomAccess geo_{0, nullptr, nullptr};
+  void* geo_a_ = nullptr;
+  void* geo_b_ = nullptr;
+  i64 geo_bytes_ = 0;
+  bool general_ = false;
   int smem_ = 0, vgrid_ = 0;
   T *x_ = nullptr, *r_ = nullptr, *p_ = nullptr, *v_ = nullptr, *z_ = nullptr, *minv_ = nullptr;
   double *partials_a_ = nullptr, *partials_b_ = nullptr, *d_history_ = nullptr;
@@ -509,6 +666,6 @@ int Engine<P, T>::solve(const mfcg_solve_args* a, mfcg_solve_result* res) {
   return MFCG_OK;
 }
 
-EngineBase* make_engine(OpCommon* c);  // dispatch over (degree, precision), mfcg_b200.cu
+EngineBase* make_engine(OpCommon* c, int* status);  // dispatch over (degree, precision), mfcg_b200.cu
 
 }  // namespace mfcg

@@ -11,14 +11,14 @@ namespace mfcg {
 #define MFCG_CAT2(a, b) a##b
 #define MFCG_CAT(a, b) MFCG_CAT2(a, b)
 
-EngineBase* MFCG_CAT(make_engine_p, MFCG_P)(OpCommon* c) {
+EngineBase* MFCG_CAT(make_engine_p, MFCG_P)(OpCommon* c, int* status) {
   if (c->precision == 0) {
     auto* e = new Engine<MFCG_P, double>(c);
-    if (e->init() != MFCG_OK) { delete e; return nullptr; }
+    if ((*status = e->init()) != MFCG_OK) { delete e; return nullptr; }
     return e;
   }
   auto* e = new Engine<MFCG_P, float>(c);
-  if (e->init() != MFCG_OK) { delete e; return nullptr; }
+  if ((*status = e->init()) != MFCG_OK) { delete e; return nullptr; }
   return e;
 }
 

@@ -76,17 +76,19 @@ struct SolveState {
 // NT_C "math" threads (TPC per cell) (sum-factorisation sweeps, shared memory only), NT_P
 // "memory" threads (all global loads: pre on the way in, post one layer behind),
 // KC points per load batch of a memory thread (memory-level parallelism).
-template <int P> struct Cfg;
-#define MFCG_CFG(P_, B_, TPC_, TP_, KC_, MB_)                                                  \
-  template <> struct Cfg<P_> {                                                                 \
-    static constexpr int BX = B_, BY = B_, TPC = TPC_, NT_P = TP_, KC = KC_, MINB = MB_,       \
-                         NT_C = ((B_ * B_ * TPC_ + 31) / 32) * 32, THREADS = NT_C + TP_;       \
+template <int P, int G = 0> struct Cfg;
+#define MFCG_CFG(P_, G_, BX_, BY_, TPC_, TP_, KC_, MB_)                                        \
+  template <> struct Cfg<P_, G_> {                                                             \
+    static constexpr int BX = BX_, BY = BY_, TPC = TPC_, NT_P = TP_, KC = KC_, MINB = MB_,     \
+                         NT_C = ((BX_ * BY_ * TPC_ + 31) / 32) * 32, THREADS = NT_C + TP_;     \
   };
-// TPC = math threads per cell; each owns ceil((P+1)^2 / TPC) lines of that cell in every sweep
-MFCG_CFG(1, 16, 1, 256, 3, 2)
-MFCG_CFG(2, 10, 3, 192, 3, 2)
-MFCG_CFG(3, 6, 8, 224, 3, 2)
-MFCG_CFG(4, 5, 9, 288, 3, 2)
+// TPC = math threads per cell; each owns ceil((P+1)^2 / TPC) lines of that cell in every sweep.
+// G = 0: separable cell operator on affine meshes (two tiles per cell);
+// G = 1: general coefficient tensor per quadrature point (three tiles per cell, smaller bricks).
+MFCG_CFG(1, 0, 16, 16, 1, 256, 3, 2)
+MFCG_CFG(2, 0, 10, 10, 3, 192, 3, 2)
+MFCG_CFG(3, 0, 6, 6, 8, 224, 3, 2)
+MFCG_CFG(4, 0, 5, 5, 9, 288, 3, 2)
 #ifndef MFCG_KC5
 #define MFCG_KC5 3
 #endif
@@ -96,21 +98,30 @@ MFCG_CFG(4, 5, 9, 288, 3, 2)
 #ifndef MFCG_NTP5
 #define MFCG_NTP5 320
 #endif
-MFCG_CFG(5, 4, MFCG_TPC5, MFCG_NTP5, MFCG_KC5, 2)
-MFCG_CFG(6, 3, 25, 256, 3, 2)
-MFCG_CFG(7, 2, 32, 256, 3, 2)
-MFCG_CFG(8, 2, 32, 256, 3, 2)
+MFCG_CFG(5, 0, 4, 4, MFCG_TPC5, MFCG_NTP5, MFCG_KC5, 2)
+MFCG_CFG(6, 0, 3, 3, 25, 256, 3, 2)
+MFCG_CFG(7, 0, 2, 2, 32, 256, 3, 2)
+MFCG_CFG(8, 0, 2, 2, 32, 256, 3, 2)
+MFCG_CFG(1, 1, 16, 16, 1, 256, 3, 2)
+MFCG_CFG(2, 1, 10, 10, 3, 192, 3, 2)
+MFCG_CFG(3, 1, 6, 6, 8, 224, 3, 2)
+MFCG_CFG(4, 1, 5, 5, 9, 288, 3, 2)
+MFCG_CFG(5, 1, 4, 3, 12, 224, 3, 2)
+MFCG_CFG(6, 1, 3, 2, 25, 224, 3, 2)
+MFCG_CFG(7, 1, 2, 2, 32, 256, 3, 2)
+MFCG_CFG(8, 1, 2, 2, 32, 256, 3, 2)
 
-template <int P> struct Geo {
+template <int P, int G = 0> struct Geo {
   static constexpr int N = P + 1;
   static constexpr int RS = (N % 2 == 0) ? N + 1 : N;  // odd row stride: conflict-free 64-bit columns
   static constexpr int TILE = N * N * RS;
-  static constexpr int NCELL = Cfg<P>::BX * Cfg<P>::BY;
-  static constexpr int WX = P * Cfg<P>::BX + 1;         // window row stride (odd for every Cfg)
-  static constexpr int PLANE = WX * (P * Cfg<P>::BY + 1);
+  static constexpr int NTILE = G ? 3 : 2;               // scratch tiles per cell
+  static constexpr int NCELL = Cfg<P, G>::BX * Cfg<P, G>::BY;
+  static constexpr int WX = (P * Cfg<P, G>::BX + 1) | 1; // window row stride, odd
+  static constexpr int PLANE = WX * (P * Cfg<P, G>::BY + 1);
   static constexpr int RB = 2 * P + 1;                  // lattice planes in the ring: two layers share one
   template <typename T> __host__ __device__ static constexpr size_t red_offset() {
-    return (256 + sizeof(T) * (size_t)(RB * PLANE + PLANE + 2 * NCELL * TILE) + 15) & ~(size_t)15;
+    return (256 + sizeof(T) * (size_t)(RB * PLANE + PLANE + NTILE * NCELL * TILE) + 15) & ~(size_t)15;
   }
   template <typename T> __host__ __device__ static constexpr size_t smem_bytes() { return red_offset<T>() + 8 * 7 * 32; }
 };
@@ -191,6 +202,110 @@ __device__ __forceinline__ void block_reduce7_store(double* s, double* red, doub
     for (int i = 0; i < nw; ++i) acc += red[i * 7 + threadIdx.x];
     out_row[threadIdx.x] = acc;
   }
+}
+
+// ---------------------------------------------------------------------------
+// General geometry (curved meshes): per quadrature point the symmetric coefficient tensor
+// G = J^-1 (w det J) J^-T (operator.py:202-249, mesh.py:194-201 storage xx,yy,zz,xy,xz,yz).
+// The cell kernel interpolates to the n_q = p+1 quadrature points (S, centro-symmetric),
+// differentiates there with the collocation derivative Dc (anti-centro-symmetric; Dc S = D up
+// to rounding, tensor.py: the 9+9 sweeps of evaluate/integrate_gradients collapse to 12),
+// applies G, and transposes.  Even/odd halves, row-major, not symmetric:
+//   Se[q][i] = (S[q][i] + S[q][N-1-i])/2 (middle column S[q][H]),  So[q][i] = (S[q][i] - S[q][N-1-i])/2,
+//   Be[q][r] = (Dc[q][r] + Dc[q][N-1-r])/2 (middle column Dc[q][H]), Bo[q][r] = (Dc[q][r] - Dc[q][N-1-r])/2.
+template <typename T, int N> struct GenTables {
+  static constexpr int H = N / 2, HE = (N + 1) / 2;
+  T Se[HE * HE], So[(H > 0 ? H : 1) * (H > 0 ? H : 1)], Be[(H > 0 ? H : 1) * HE], Bo[HE * (H > 0 ? H : 1)];
+  T qv[N * 3], qd[N * 3];  // quadratic Lagrange basis on {0,1/2,1} and its derivative at the quadrature points
+  T w3[N];                 // quadrature weights (quadratic_compute builds w_q det J itself)
+};
+struct GeomAccess {
+  int kind;              // MFCG_GEOM_*: 1 final tensor, 2 inverse Jacobian + jxw, 3 27 nodes per cell
+  const void* data;      // [n_cells][nq^3][6] | [n_cells][nq^3][9] | [n_cells][27][3]
+  const void* jxw;       // kind 2: [n_cells][nq^3]
+};
+
+// out = A u for centro-symmetric A given by halves (transposed = apply A^T)
+template <int N, typename T>
+__device__ __forceinline__ void eo_apply_sym(const T* Ae, const T* Ao, bool transposed, const T* e, const T* o, T* se, T* so) {
+  constexpr int H = EOShape<N>::H, HE = EOShape<N>::HE;
+#pragma unroll
+  for (int i = 0; i < HE; ++i) {
+    T a = 0;
+#pragma unroll
+    for (int j = 0; j < HE; ++j) a += (transposed ? Ae[j * HE + i] : Ae[i * HE + j]) * e[j];
+    se[i] = a;
+  }
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    T a = 0;
+#pragma unroll
+    for (int j = 0; j < H; ++j) a += (transposed ? Ao[j * H + i] : Ao[i * H + j]) * o[j];
+    so[i] = a;
+  }
+}
+// out = Dc u (or Dc^T u) for anti-centro-symmetric Dc: even output from odd input and vice versa.
+// Be is H x HE (rows q < H), Bo is HE x H (rows q < HE).
+template <int N, typename T>
+__device__ __forceinline__ void eo_apply_anti(const T* Be, const T* Bo, bool transposed, const T* e, const T* o, T* se, T* so) {
+  constexpr int H = EOShape<N>::H, HE = EOShape<N>::HE;
+#pragma unroll
+  for (int i = 0; i < HE; ++i) {  // even part of the output
+    T a = 0;
+#pragma unroll
+    for (int j = 0; j < H; ++j) a += (transposed ? Be[j * HE + i] : Bo[i * H + j]) * o[j];
+    se[i] = a;
+  }
+#pragma unroll
+  for (int i = 0; i < H; ++i) {   // odd part of the output
+    T a = 0;
+#pragma unroll
+    for (int j = 0; j < HE; ++j) a += (transposed ? Bo[j * H + i] : Be[i * HE + j]) * e[j];
+    so[i] = a;
+  }
+}
+
+// Jacobian of the tri-quadratic cell map at one point from the 27 nodes (x fastest),
+// J[i][j] = d x_i / d xi_j (mesh.py:155-174), given the 1D quadratic basis values/derivatives
+// (3 each) in every direction.
+__device__ __forceinline__ void jacobian27(const double* nodes, const double* vx, const double* dx, const double* vy,
+                                           const double* dy, const double* vz, const double* dz, double* J) {
+#pragma unroll
+  for (int t = 0; t < 9; ++t) J[t] = 0.0;
+  for (int c = 0; c < 3; ++c)
+    for (int b = 0; b < 3; ++b) {
+      const double vv = vy[b] * vz[c], dyv = dy[b] * vz[c], dzv = vy[b] * dz[c];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double* nd = nodes + 3 * ((c * 3 + b) * 3 + a);
+        const double wx = dx[a] * vv, wy = vx[a] * dyv, wz = vx[a] * dzv;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          J[i * 3 + 0] += nd[i] * wx;
+          J[i * 3 + 1] += nd[i] * wy;
+          J[i * 3 + 2] += nd[i] * wz;
+        }
+      }
+    }
+}
+// inverse and determinant of a 3x3 matrix
+__device__ __forceinline__ double invert3(const double* J, double* inv) {
+  const double c00 = J[4] * J[8] - J[5] * J[7], c01 = J[5] * J[6] - J[3] * J[8], c02 = J[3] * J[7] - J[4] * J[6];
+  const double det = J[0] * c00 + J[1] * c01 + J[2] * c02;
+  const double id = 1.0 / det;
+  inv[0] = c00 * id; inv[1] = (J[2] * J[7] - J[1] * J[8]) * id; inv[2] = (J[1] * J[5] - J[2] * J[4]) * id;
+  inv[3] = c01 * id; inv[4] = (J[0] * J[8] - J[2] * J[6]) * id; inv[5] = (J[2] * J[3] - J[0] * J[5]) * id;
+  inv[6] = c02 * id; inv[7] = (J[1] * J[6] - J[0] * J[7]) * id; inv[8] = (J[0] * J[4] - J[1] * J[3]) * id;
+  return det;
+}
+// G = inv (jxw) inv^T, 6-storage
+__device__ __forceinline__ void tensor6(const double* inv, double jxw, double* g) {
+  g[0] = jxw * (inv[0] * inv[0] + inv[1] * inv[1] + inv[2] * inv[2]);
+  g[1] = jxw * (inv[3] * inv[3] + inv[4] * inv[4] + inv[5] * inv[5]);
+  g[2] = jxw * (inv[6] * inv[6] + inv[7] * inv[7] + inv[8] * inv[8]);
+  g[3] = jxw * (inv[0] * inv[3] + inv[1] * inv[4] + inv[2] * inv[5]);
+  g[4] = jxw * (inv[0] * inv[6] + inv[1] * inv[7] + inv[2] * inv[8]);
+  g[5] = jxw * (inv[3] * inv[6] + inv[4] * inv[7] + inv[5] * inv[8]);
 }
 
 // ---------------------------------------------------------------------------
@@ -281,14 +396,15 @@ template <int COUNT> __device__ __forceinline__ void math_barrier() {
 //                 memory, a deterministic gather of the cells' contributions per
 //                 lattice point, v stored (interior) or atomically added (shared).
 // Hand-over through two mbarrier pairs (full/empty per layer parity).
-template <int P, typename T, int MODE>
-__global__ void __launch_bounds__(Cfg<P>::THREADS, Cfg<P>::MINB)
-k_brick(BrickGrid g, SepTables<T, P + 1> tab, const T* __restrict__ src, T* __restrict__ Pv,
+template <int P, typename T, int MODE, int G>
+__global__ void __launch_bounds__(Cfg<P, G>::THREADS, Cfg<P, G>::MINB)
+k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAccess geo,
+        const T* __restrict__ src, T* __restrict__ Pv,
         T* __restrict__ V, T* __restrict__ R, T* __restrict__ X, const T* __restrict__ Minv,
         const SolveState* __restrict__ st, double* __restrict__ partials) {
-  constexpr int N = P + 1, RS = Geo<P>::RS, TILE = Geo<P>::TILE, WX = Geo<P>::WX,
-                PLANE = Geo<P>::PLANE, NCELL = Geo<P>::NCELL, RB = Geo<P>::RB,
-                NT_C = Cfg<P>::NT_C, NT_P = Cfg<P>::NT_P, KC = Cfg<P>::KC, HE = EOShape<N>::HE;
+  constexpr int N = P + 1, RS = Geo<P, G>::RS, TILE = Geo<P, G>::TILE, WX = Geo<P, G>::WX,
+                PLANE = Geo<P, G>::PLANE, NCELL = Geo<P, G>::NCELL, RB = Geo<P, G>::RB,
+                NT_C = Cfg<P, G>::NT_C, NT_P = Cfg<P, G>::NT_P, KC = Cfg<P, G>::KC, HE = EOShape<N>::HE;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   i64* st27 = reinterpret_cast<i64*>(smem_raw);                               // 27 entity starts
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem_raw + 224);  // full[2], empty[2]
@@ -296,7 +412,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, const T* __restrict__ src, T* __re
   T* carry = ring + RB * PLANE;
   T* A = carry + PLANE;
   T* Bs = A + NCELL * TILE;
-  constexpr size_t RED_OFF = Geo<P>::template red_offset<T>();
+  constexpr size_t RED_OFF = Geo<P, G>::template red_offset<T>();
   double* red = reinterpret_cast<double*>(smem_raw + RED_OFF);
 
 #ifdef MFCG_TIMING
@@ -514,7 +630,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, const T* __restrict__ src, T* __re
     // ===================== math warps =====================
     // Fixed ownership: TPC threads per cell, thread q of a cell owns lines q, q+TPC, ... of
     // that cell in every sweep of every layer, so all index arithmetic is hoisted.
-    constexpr int TPC = Cfg<P>::TPC, LPT = (N * N + TPC - 1) / TPC;
+    constexpr int TPC = Cfg<P, G>::TPC, LPT = (N * N + TPC - 1) / TPC;
     const int cell = tid / TPC, q = tid - cell * TPC;
     const bool has_cell = cell < bcx * bcy;
     const int cy = has_cell ? cell / bcx : 0, cx = has_cell ? cell - cy * bcx : 0;
@@ -529,112 +645,250 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, const T* __restrict__ src, T* __re
       mbar_wait(&bars[stage], (L >> 1) & 1);  // layer L full
       MFCG_TOC(tc, 4);
 
-      // ---- x sweep: a = M u, b = gx K u along every x line of the cell
-      if (has_cell && !(MFCG_SKIP & 1)) {
+      if (G == 1) {
+        // ===== general coefficient tensor: 12 sweeps + pointwise flux (operator.py:253-281) =====
+        T* const Ct = Bs + NCELL * TILE + cell * TILE;  // third tile of the cell
+        // line l of a sweep direction: base offset and element stride inside a tile
+        //   x lines (k,j): l*RS, 1;  y lines (k,i): k*N*RS + i, RS;  z lines (j,i): j*RS + i, N*RS
+        auto line_base = [&](int dir, int l) {
+          const int hi = l / N, lo = l - hi * N;
+          return dir == 0 ? l * RS : (dir == 1 ? hi * N * RS + lo : hi * RS + lo);
+        };
+        constexpr int STR[3] = {1, RS, N * RS};
+        // out-of-place or in-place 1D operator on the owned lines of direction dir
+        auto sweep = [&](int dir, int kind, bool tr, bool acc, const T* srct, int sstride_unused, T* dstt) {
+          (void)sstride_unused;
+          if (!has_cell || (MFCG_SKIP & 1)) return;
 #pragma unroll 1
-        for (int t = 0; t < LPT; ++t) {
-          const int l = LineOrder<N>::x(q + t * TPC, TPC);
-          if (l < 0) continue;
-          const int k = l / N, j = l - k * N;
-          int slot = s0 + k;
-          if (slot >= RB) slot -= RB;
-          const T* row = ring_cell + slot * PLANE + j * WX;
-          T u[N], e[HE], o[HE];
+          for (int t = 0; t < LPT; ++t) {
+            const int l = q + t * TPC;
+            if (l >= N * N) break;
+            const int base = line_base(dir, l);
+            const int str = dir == 0 ? STR[0] : (dir == 1 ? STR[1] : STR[2]);
+            T u[N], e[HE], o[HE], se[HE], so[HE], out[N];
 #pragma unroll
-          for (int i = 0; i < N; ++i) u[i] = row[i];
-          eo_split<N>(u, e, o);
-          T* ao = At + l * RS;
-          T* bo = Bt + l * RS;
-          T se[HE], so[HE], out[N];
+            for (int i = 0; i < N; ++i) u[i] = srct[base + i * str];
+            eo_split<N>(u, e, o);
+            if (kind == 0) eo_apply_sym<N>(gen.Se, gen.So, tr, e, o, se, so);
+            else eo_apply_anti<N>(gen.Be, gen.Bo, tr, e, o, se, so);
+            eo_join<N>(se, so, out);
 #pragma unroll
-          for (int i = 0; i < HE; ++i) { se[i] = 0; so[i] = 0; }
-          eo_mul<N>(tab.Me, tab.Mo, e, o, se, so);
-          eo_join<N>(se, so, out);
+            for (int i = 0; i < N; ++i) {
+              if (acc) dstt[base + i * str] += out[i];
+              else dstt[base + i * str] = out[i];
+            }
+          }
+        };
+        // 1. interpolate to the quadrature points: x from the ring, then y, z in place
+        if (has_cell && !(MFCG_SKIP & 1)) {
+#pragma unroll 1
+          for (int t = 0; t < LPT; ++t) {
+            const int l = q + t * TPC;
+            if (l >= N * N) break;
+            const int k = l / N, j = l - k * N;
+            int slot = s0 + k;
+            if (slot >= RB) slot -= RB;
+            const T* row = ring_cell + slot * PLANE + j * WX;
+            T u[N], e[HE], o[HE], se[HE], so[HE], out[N];
 #pragma unroll
-          for (int i = 0; i < N; ++i) ao[i] = out[i];
+            for (int i = 0; i < N; ++i) u[i] = row[i];
+            eo_split<N>(u, e, o);
+            eo_apply_sym<N>(gen.Se, gen.So, false, e, o, se, so);
+            eo_join<N>(se, so, out);
 #pragma unroll
-          for (int i = 0; i < HE; ++i) { se[i] = 0; so[i] = 0; }
-          eo_mul<N>(tab.Ke, tab.Ko, e, o, se, so);
-#pragma unroll
-          for (int i = 0; i < HE; ++i) { se[i] *= tab.g[0]; so[i] *= tab.g[0]; }
-          eo_join<N>(se, so, out);
-#pragma unroll
-          for (int i = 0; i < N; ++i) bo[i] = out[i];
+            for (int i = 0; i < N; ++i) At[l * RS + i] = out[i];
+          }
         }
-      }
-      MFCG_TOC(tc, 5);
-      math_barrier<NT_C>();
-      MFCG_TOC(tc, 8);
+        math_barrier<NT_C>();
+        sweep(1, 0, false, false, At, 0, At);
+        math_barrier<NT_C>();
+        sweep(2, 0, false, false, At, 0, At);
+        math_barrier<NT_C>();
+        // 2. reference-space gradient at the quadrature points: x -> Bt, y -> Ct (z in registers below)
+        sweep(0, 1, false, false, At, 0, Bt);
+        sweep(1, 1, false, false, At, 0, Ct);
+        math_barrier<NT_C>();
+        // 3. per z column: gz, flux = G grad at every point, z part of the transposed gradient
+        if (has_cell && !(MFCG_SKIP & 1)) {
+          const i64 cellg = ((i64)(mz * g.B[2] + L) * g.cells[1] + (my * g.B[1] + cy)) * g.cells[0] + (mx * g.B[0] + cx);
+          constexpr int NQ3 = N * N * N;
+#pragma unroll 1
+          for (int t = 0; t < LPT; ++t) {
+            const int l = q + t * TPC;
+            if (l >= N * N) break;
+            const int j = l / N, i = l - j * N;
+            const int base = j * RS + i;
+            T u[N], e[HE], o[HE], se[HE], so[HE], gz[N], fz[N];
+#pragma unroll
+            for (int k = 0; k < N; ++k) u[k] = At[base + k * N * RS];
+            eo_split<N>(u, e, o);
+            eo_apply_anti<N>(gen.Be, gen.Bo, false, e, o, se, so);
+            eo_join<N>(se, so, gz);
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+              const int qp = (k * N + j) * N + i;
+              T G6[6];
+              if (geo.kind == 1) {
+                const T* gp = reinterpret_cast<const T*>(geo.data) + ((i64)cellg * NQ3 + qp) * 6;
+#pragma unroll
+                for (int c = 0; c < 6; ++c) G6[c] = gp[c];
+              } else {
+                double inv[9], jxw, g6d[6];
+                if (geo.kind == 2) {
+                  const T* ip = reinterpret_cast<const T*>(geo.data) + ((i64)cellg * NQ3 + qp) * 9;
+#pragma unroll
+                  for (int c = 0; c < 9; ++c) inv[c] = (double)ip[c];
+                  jxw = (double)reinterpret_cast<const T*>(geo.jxw)[(i64)cellg * NQ3 + qp];
+                } else {
+                  const double* nd = reinterpret_cast<const double*>(geo.data) + (i64)cellg * 81;
+                  double vx[3], dx[3], vy[3], dy[3], vz[3], dz[3], J[9];
+#pragma unroll
+                  for (int c = 0; c < 3; ++c) {
+                    vx[c] = (double)gen.qv[i * 3 + c]; dx[c] = (double)gen.qd[i * 3 + c];
+                    vy[c] = (double)gen.qv[j * 3 + c]; dy[c] = (double)gen.qd[j * 3 + c];
+                    vz[c] = (double)gen.qv[k * 3 + c]; dz[c] = (double)gen.qd[k * 3 + c];
+                  }
+                  jacobian27(nd, vx, dx, vy, dy, vz, dz, J);
+                  const double det = invert3(J, inv);
+                  jxw = det * (double)gen.w3[i] * (double)gen.w3[j] * (double)gen.w3[k];
+                }
+                tensor6(inv, jxw, g6d);
+#pragma unroll
+                for (int c = 0; c < 6; ++c) G6[c] = (T)g6d[c];
+              }
+              const T gx = Bt[base + k * N * RS], gy = Ct[base + k * N * RS], gzz = gz[k];
+              Bt[base + k * N * RS] = G6[0] * gx + G6[3] * gy + G6[4] * gzz;
+              Ct[base + k * N * RS] = G6[3] * gx + G6[1] * gy + G6[5] * gzz;
+              fz[k] = G6[4] * gx + G6[5] * gy + G6[2] * gzz;
+            }
+            eo_split<N>(fz, e, o);
+            eo_apply_anti<N>(gen.Be, gen.Bo, true, e, o, se, so);
+            eo_join<N>(se, so, u);
+#pragma unroll
+            for (int k = 0; k < N; ++k) At[base + k * N * RS] = u[k];
+          }
+        }
+        math_barrier<NT_C>();
+        // 4. remaining transposed gradient parts accumulate into At, then integrate (S^T) x, y, z
+        sweep(0, 1, true, true, Bt, 0, At);
+        math_barrier<NT_C>();
+        sweep(1, 1, true, true, Ct, 0, At);
+        math_barrier<NT_C>();
+        sweep(0, 0, true, false, At, 0, At);
+        math_barrier<NT_C>();
+        sweep(1, 0, true, false, At, 0, At);
+        math_barrier<NT_C>();
+        sweep(2, 0, true, false, At, 0, At);
+        math_barrier<NT_C>();
+      } else {
+        // ---- x sweep: a = M u, b = gx K u along every x line of the cell
+        if (has_cell && !(MFCG_SKIP & 1)) {
+  #pragma unroll 1
+          for (int t = 0; t < LPT; ++t) {
+            const int l = LineOrder<N>::x(q + t * TPC, TPC);
+            if (l < 0) continue;
+            const int k = l / N, j = l - k * N;
+            int slot = s0 + k;
+            if (slot >= RB) slot -= RB;
+            const T* row = ring_cell + slot * PLANE + j * WX;
+            T u[N], e[HE], o[HE];
+  #pragma unroll
+            for (int i = 0; i < N; ++i) u[i] = row[i];
+            eo_split<N>(u, e, o);
+            T* ao = At + l * RS;
+            T* bo = Bt + l * RS;
+            T se[HE], so[HE], out[N];
+  #pragma unroll
+            for (int i = 0; i < HE; ++i) { se[i] = 0; so[i] = 0; }
+            eo_mul<N>(tab.Me, tab.Mo, e, o, se, so);
+            eo_join<N>(se, so, out);
+  #pragma unroll
+            for (int i = 0; i < N; ++i) ao[i] = out[i];
+  #pragma unroll
+            for (int i = 0; i < HE; ++i) { se[i] = 0; so[i] = 0; }
+            eo_mul<N>(tab.Ke, tab.Ko, e, o, se, so);
+  #pragma unroll
+            for (int i = 0; i < HE; ++i) { se[i] *= tab.g[0]; so[i] *= tab.g[0]; }
+            eo_join<N>(se, so, out);
+  #pragma unroll
+            for (int i = 0; i < N; ++i) bo[i] = out[i];
+          }
+        }
+        MFCG_TOC(tc, 5);
+        math_barrier<NT_C>();
+        MFCG_TOC(tc, 8);
 
-      // ---- y sweep (in place): c = M a, de = gy K a + M b
-      if (has_cell && !(MFCG_SKIP & 1)) {
-#pragma unroll 1
-        for (int t = 0; t < LPT; ++t) {
-          const int l = LineOrder<N>::y(q + t * TPC, TPC);
-          if (l < 0) continue;
-          const int k = l / N, i = l - k * N;
-          T* ac = At + k * N * RS + i;
-          T* bc = Bt + k * N * RS + i;
-          T a[N], ea[HE], oa[HE], eb[HE], ob[HE];
-#pragma unroll
-          for (int j = 0; j < N; ++j) a[j] = ac[j * RS];
-          eo_split<N>(a, ea, oa);
-#pragma unroll
-          for (int j = 0; j < N; ++j) a[j] = bc[j * RS];
-          eo_split<N>(a, eb, ob);
-          T se[HE], so[HE], out[N];
-#pragma unroll
-          for (int i2 = 0; i2 < HE; ++i2) { se[i2] = 0; so[i2] = 0; }
-          eo_mul<N>(tab.Ke, tab.Ko, ea, oa, se, so);  // K a
-#pragma unroll
-          for (int i2 = 0; i2 < HE; ++i2) { se[i2] *= tab.g[1]; so[i2] *= tab.g[1]; }
-          eo_mul<N>(tab.Me, tab.Mo, eb, ob, se, so);  // + M b
-          eo_join<N>(se, so, out);
-#pragma unroll
-          for (int j = 0; j < N; ++j) bc[j * RS] = out[j];
-#pragma unroll
-          for (int i2 = 0; i2 < HE; ++i2) { se[i2] = 0; so[i2] = 0; }
-          eo_mul<N>(tab.Me, tab.Mo, ea, oa, se, so);  // c = M a
-          eo_join<N>(se, so, out);
-#pragma unroll
-          for (int j = 0; j < N; ++j) ac[j * RS] = out[j];
+        // ---- y sweep (in place): c = M a, de = gy K a + M b
+        if (has_cell && !(MFCG_SKIP & 1)) {
+  #pragma unroll 1
+          for (int t = 0; t < LPT; ++t) {
+            const int l = LineOrder<N>::y(q + t * TPC, TPC);
+            if (l < 0) continue;
+            const int k = l / N, i = l - k * N;
+            T* ac = At + k * N * RS + i;
+            T* bc = Bt + k * N * RS + i;
+            T a[N], ea[HE], oa[HE], eb[HE], ob[HE];
+  #pragma unroll
+            for (int j = 0; j < N; ++j) a[j] = ac[j * RS];
+            eo_split<N>(a, ea, oa);
+  #pragma unroll
+            for (int j = 0; j < N; ++j) a[j] = bc[j * RS];
+            eo_split<N>(a, eb, ob);
+            T se[HE], so[HE], out[N];
+  #pragma unroll
+            for (int i2 = 0; i2 < HE; ++i2) { se[i2] = 0; so[i2] = 0; }
+            eo_mul<N>(tab.Ke, tab.Ko, ea, oa, se, so);  // K a
+  #pragma unroll
+            for (int i2 = 0; i2 < HE; ++i2) { se[i2] *= tab.g[1]; so[i2] *= tab.g[1]; }
+            eo_mul<N>(tab.Me, tab.Mo, eb, ob, se, so);  // + M b
+            eo_join<N>(se, so, out);
+  #pragma unroll
+            for (int j = 0; j < N; ++j) bc[j * RS] = out[j];
+  #pragma unroll
+            for (int i2 = 0; i2 < HE; ++i2) { se[i2] = 0; so[i2] = 0; }
+            eo_mul<N>(tab.Me, tab.Mo, ea, oa, se, so);  // c = M a
+            eo_join<N>(se, so, out);
+  #pragma unroll
+            for (int j = 0; j < N; ++j) ac[j * RS] = out[j];
+          }
         }
-      }
-      MFCG_TOC(tc, 6);
-      math_barrier<NT_C>();
-      MFCG_TOC(tc, 8);
+        MFCG_TOC(tc, 6);
+        math_barrier<NT_C>();
+        MFCG_TOC(tc, 8);
 
-      // ---- z sweep: out = M de + gz K c, written over c
-      if (has_cell && !(MFCG_SKIP & 1)) {
-#pragma unroll 1
-        for (int t = 0; t < LPT; ++t) {
-          const int l = LineOrder<N>::z(q + t * TPC, TPC);
-          if (l < 0) continue;
-          const int j = l / N, i = l - j * N;
-          T* ac = At + j * RS + i;
-          const T* bc = Bt + j * RS + i;
-          T a[N], ec[HE], oc[HE], ed[HE], od[HE];
-#pragma unroll
-          for (int k = 0; k < N; ++k) a[k] = ac[k * N * RS];
-          eo_split<N>(a, ec, oc);
-#pragma unroll
-          for (int k = 0; k < N; ++k) a[k] = bc[k * N * RS];
-          eo_split<N>(a, ed, od);
-          T se[HE], so[HE], out[N];
-#pragma unroll
-          for (int i2 = 0; i2 < HE; ++i2) { se[i2] = 0; so[i2] = 0; }
-          eo_mul<N>(tab.Ke, tab.Ko, ec, oc, se, so);  // K c
-#pragma unroll
-          for (int i2 = 0; i2 < HE; ++i2) { se[i2] *= tab.g[2]; so[i2] *= tab.g[2]; }
-          eo_mul<N>(tab.Me, tab.Mo, ed, od, se, so);  // + M de
-          eo_join<N>(se, so, out);
-#pragma unroll
-          for (int k = 0; k < N; ++k) ac[k * N * RS] = out[k];
+        // ---- z sweep: out = M de + gz K c, written over c
+        if (has_cell && !(MFCG_SKIP & 1)) {
+  #pragma unroll 1
+          for (int t = 0; t < LPT; ++t) {
+            const int l = LineOrder<N>::z(q + t * TPC, TPC);
+            if (l < 0) continue;
+            const int j = l / N, i = l - j * N;
+            T* ac = At + j * RS + i;
+            const T* bc = Bt + j * RS + i;
+            T a[N], ec[HE], oc[HE], ed[HE], od[HE];
+  #pragma unroll
+            for (int k = 0; k < N; ++k) a[k] = ac[k * N * RS];
+            eo_split<N>(a, ec, oc);
+  #pragma unroll
+            for (int k = 0; k < N; ++k) a[k] = bc[k * N * RS];
+            eo_split<N>(a, ed, od);
+            T se[HE], so[HE], out[N];
+  #pragma unroll
+            for (int i2 = 0; i2 < HE; ++i2) { se[i2] = 0; so[i2] = 0; }
+            eo_mul<N>(tab.Ke, tab.Ko, ec, oc, se, so);  // K c
+  #pragma unroll
+            for (int i2 = 0; i2 < HE; ++i2) { se[i2] *= tab.g[2]; so[i2] *= tab.g[2]; }
+            eo_mul<N>(tab.Me, tab.Mo, ed, od, se, so);  // + M de
+            eo_join<N>(se, so, out);
+  #pragma unroll
+            for (int k = 0; k < N; ++k) ac[k * N * RS] = out[k];
+          }
         }
+        MFCG_TOC(tc, 7);
+        math_barrier<NT_C>();
+        MFCG_TOC(tc, 8);
+
       }
-      MFCG_TOC(tc, 7);
-      math_barrier<NT_C>();
-      MFCG_TOC(tc, 8);
 
       // ---- gather the cells' contributions per lattice point, finish the planes
       for (int rem = tid; rem < ((MFCG_SKIP & 2) ? 0 : fp); rem += NT_C) {
@@ -1089,6 +1343,113 @@ template <typename T>
 __global__ void k_fill(i64 n, T* __restrict__ out, T value) {
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
     out[i] = value;
+}
+
+
+// ---------------------------------------------------------------------------
+// Geometry set-up on the device (mesh.py:126-174, 194-252).  One block per cell: the 27
+// tri-quadratic nodes of the cell are the sine-bump map of the {0,1/2,1}^3 lattice
+// (mesh.py:73-80), then every thread evaluates Jacobians at tensor points.
+struct GeoMesh {
+  int cells[3];
+  double h[3], ext[3], amp;
+};
+struct PointTab {   // quadratic basis on {0,1/2,1} at up to 10 1D points, and their weights
+  double qv[30], qd[30], w[10];
+  int n;
+};
+
+__device__ __forceinline__ void cell_nodes_to_smem(const GeoMesh& gm, i64 cell, double* nodes /*[81]*/) {
+  const int cx = (int)(cell % gm.cells[0]), cy = (int)((cell / gm.cells[0]) % gm.cells[1]),
+            cz = (int)(cell / ((i64)gm.cells[0] * gm.cells[1]));
+  const double kPi = 3.14159265358979323846;
+  if (threadIdx.x < 27) {
+    const int a = threadIdx.x % 3, b = (threadIdx.x / 3) % 3, c = threadIdx.x / 9;
+    const double X = cx * gm.h[0] + (0.5 * a) * gm.h[0], Y = cy * gm.h[1] + (0.5 * b) * gm.h[1],
+                 Z = cz * gm.h[2] + (0.5 * c) * gm.h[2];
+    double bump = 0.0;
+    if (gm.amp != 0.0)
+      bump = gm.amp * (sin(kPi * X / gm.ext[0]) * sin(kPi * Y / gm.ext[1]) * sin(kPi * Z / gm.ext[2]));
+    nodes[threadIdx.x * 3 + 0] = X + bump;
+    nodes[threadIdx.x * 3 + 1] = Y + bump;
+    nodes[threadIdx.x * 3 + 2] = Z + bump;
+  }
+}
+
+// kind 1: a = final tensor [cell][q][6]; kind 2: a = inverse Jacobian [cell][q][9], b = jxw [cell][q];
+// kind 3: a = nodes [cell][27][3] (always double).  error: 1 if some det J <= 0 (mesh.py:171-172).
+template <typename T>
+__global__ void k_geometry(GeoMesh gm, PointTab pt, i64 n_cells, int kind, T* __restrict__ a, T* __restrict__ b,
+                           double* __restrict__ nodes_out, int* __restrict__ error) {
+  __shared__ double nodes[81];
+  const int n = pt.n, nq3 = n * n * n;
+  for (i64 cell = blockIdx.x; cell < n_cells; cell += gridDim.x) {
+    __syncthreads();
+    cell_nodes_to_smem(gm, cell, nodes);
+    __syncthreads();
+    if (kind == 3) {
+      for (int t = threadIdx.x; t < 81; t += blockDim.x) nodes_out[cell * 81 + t] = nodes[t];
+      continue;
+    }
+    for (int q = threadIdx.x; q < nq3; q += blockDim.x) {
+      const int i = q % n, j = (q / n) % n, k = q / (n * n);
+      double J[9], inv[9];
+      jacobian27(nodes, pt.qv + 3 * i, pt.qd + 3 * i, pt.qv + 3 * j, pt.qd + 3 * j, pt.qv + 3 * k, pt.qd + 3 * k, J);
+      const double det = invert3(J, inv);
+      if (!(det > 0.0)) *error = 1;
+      const double jxw = det * (pt.w[k] * pt.w[j] * pt.w[i]);
+      if (kind == 1) {
+        double g6[6];
+        tensor6(inv, jxw, g6);
+        for (int c = 0; c < 6; ++c) a[(cell * nq3 + q) * 6 + c] = (T)g6[c];
+      } else {
+        for (int c = 0; c < 9; ++c) a[(cell * nq3 + q) * 9 + c] = (T)inv[c];
+        b[cell * nq3 + q] = (T)jxw;
+      }
+    }
+  }
+}
+
+// Jacobi diagonal on general geometry (operator.py:380-418): GL collocation, coefficient tensor of
+// the tri-quadratic map at the (p+1)^3 Gauss-Lobatto points of every cell.
+struct DiagGen {
+  double D2[81];  // D2[q*n+i] = Dgl[q][i]^2
+  double dd[9];   // diag of Dgl
+};
+static __global__ void k_diag_general(BrickGrid g, GeoMesh gm, PointTab pt, DiagGen dg, i64 n_cells,
+                                      double* __restrict__ diag, int* __restrict__ error) {
+  __shared__ double nodes[81];
+  extern __shared__ double Gs[];  // [n^3][6]
+  const int p = g.p, n = p + 1, n3 = n * n * n;
+  for (i64 cell = blockIdx.x; cell < n_cells; cell += gridDim.x) {
+    __syncthreads();
+    cell_nodes_to_smem(gm, cell, nodes);
+    __syncthreads();
+    for (int q = threadIdx.x; q < n3; q += blockDim.x) {
+      const int i = q % n, j = (q / n) % n, k = q / (n * n);
+      double J[9], inv[9], g6[6];
+      jacobian27(nodes, pt.qv + 3 * i, pt.qd + 3 * i, pt.qv + 3 * j, pt.qd + 3 * j, pt.qv + 3 * k, pt.qd + 3 * k, J);
+      const double det = invert3(J, inv);
+      if (!(det > 0.0)) *error = 1;
+      tensor6(inv, det * (pt.w[k] * pt.w[j] * pt.w[i]), g6);
+      for (int c = 0; c < 6; ++c) Gs[q * 6 + c] = g6[c];
+    }
+    __syncthreads();
+    const int cx = (int)(cell % g.cells[0]), cy = (int)((cell / g.cells[0]) % g.cells[1]),
+              cz = (int)(cell / ((i64)g.cells[0] * g.cells[1]));
+    for (int q = threadIdx.x; q < n3; q += blockDim.x) {
+      const int i = q % n, j = (q / n) % n, k = q / (n * n);
+      double lap = 0.0;
+      for (int t = 0; t < n; ++t) {
+        lap += dg.D2[t * n + i] * Gs[((k * n + j) * n + t) * 6 + 0];
+        lap += dg.D2[t * n + j] * Gs[((k * n + t) * n + i) * 6 + 1];
+        lap += dg.D2[t * n + k] * Gs[((t * n + j) * n + i) * 6 + 2];
+      }
+      const double* gq = Gs + q * 6;
+      lap += 2.0 * (dg.dd[i] * dg.dd[j] * gq[3] + dg.dd[i] * dg.dd[k] * gq[4] + dg.dd[j] * dg.dd[k] * gq[5]);
+      atomicAdd(&diag[lattice_to_dev(g, cx * p + i, cy * p + j, cz * p + k)], lap);
+    }
+  }
 }
 
 }  // namespace mfcg

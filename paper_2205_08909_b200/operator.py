@@ -188,6 +188,23 @@ class MatrixFreeOperator:
                 "brick": tuple(out.brick), "threads": out.threads, "smem_bytes": out.smem_bytes,
                 "geometry_bytes": out.geometry_bytes}
 
+    def device_geometry(self) -> dict:
+        """The geometry table the device built for a stored variant, under the reference's
+        payload keys (mesh.py:243-251): ``final_tensor`` (n_cells, n_q^3, 6) or
+        ``inverse_jacobian`` (n_cells, n_q^3, 3, 3) + ``jxw`` (n_cells, n_q^3)."""
+        kind = _lib.GEOMETRY_CODES[self.spec.geometry.value]
+        nc, nq3 = self.mesh.n_cells, self.spec.n_q_1d ** 3
+        if kind == 1:
+            out = np.empty(nc * nq3 * 6)
+            _lib.check(self._lib.mfcg_op_geometry(self._handle, 1, _ptr(out), out.size))
+            return {"final_tensor": out.reshape(nc, nq3, 6)}
+        if kind == 2:
+            out = np.empty(nc * nq3 * 10)
+            _lib.check(self._lib.mfcg_op_geometry(self._handle, 2, _ptr(out), out.size))
+            return {"inverse_jacobian": out[:nc * nq3 * 9].reshape(nc, nq3, 3, 3),
+                    "jxw": out[nc * nq3 * 9:].reshape(nc, nq3)}
+        raise ValueError("the operator holds no stored geometry table")
+
     def device_permutation(self) -> np.ndarray:
         """perm[user index] = index in the library's brick numbering."""
         perm = np.empty(self.n_dofs, dtype=np.int32)

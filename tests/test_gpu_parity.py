@@ -209,3 +209,61 @@ def test_all_degrees_apply_and_short_solve(p):
         res = S.solve(variant, op, b, minv=minv, config=S.SolverConfig(fixed_iterations=15))
         assert rel(hist_array(res.history), hist_array(hist)) < 1e-10, (p, variant)
         assert rel(res.x, x) < 1e-10
+
+
+# ---------------------------------------------------------------------------
+# curved meshes (BASELINE configs[2]): tri-quadratic geometry, stored and on-the-fly variants
+
+from _problems import CURVED_CASES  # noqa: E402
+
+
+@pytest.mark.parametrize("ci", [0, 1])
+def test_curved_variants_vs_reference(golden, ci):
+    S = _solvers()
+    cells, p, nq, amp = CURVED_CASES[ci]
+    g = golden["curved"]
+    m, h, plan = host_tables(cells, p, deform=amp)
+    u = g[f"k{ci}_u"]
+    ops = {}
+    for variant in ("final_tensor_load", "inverse_jacobian_load", "quadratic_compute"):
+        op = ops[variant] = gpu_operator(m, h, plan, p, nq, variant=variant)
+        # all variants describe the same map (reference tests/test_operator.py:82-88)
+        assert rel(op.apply(u), g[f"k{ci}_Au"]) < 1e-12, variant
+        assert rel(op.compute_diagonal().inverse_diagonal, g[f"k{ci}_invdiag"]) < 1e-12, variant
+    geo = ops["final_tensor_load"].device_geometry()
+    assert rel(geo["final_tensor"], g[f"k{ci}_final_tensor"]) < 1e-12
+    geo = ops["inverse_jacobian_load"].device_geometry()
+    assert rel(geo["inverse_jacobian"], g[f"k{ci}_inverse_jacobian"]) < 1e-12
+    assert rel(geo["jxw"], g[f"k{ci}_jxw"]) < 1e-12
+    b = g[f"k{ci}_b"]
+    R = g[f"k{ci}_combined_pcg_hist"]
+    for variant, op in ops.items():
+        res = S.solve("combined_pcg", op, b, minv=op.compute_diagonal(), config=S.SolverConfig(fixed_iterations=40))
+        H = hist_array(res.history)
+        assert (np.abs(H[:30, 3] - R[:30, 3]) / R[:30, 3]).max() < 1e-10, variant
+        assert rel(H[:30, :2], R[:30, :2]) < 1e-10, variant
+        assert rel(res.x, g[f"k{ci}_combined_pcg_x"]) < 1e-8, variant
+        ref = S.solve("pcg", op, b, minv=op.compute_diagonal(), config=S.SolverConfig(fixed_iterations=40))
+        assert rel(hist_array(ref.history)[:30, 3], R[:30, 3]) < 1e-8
+
+
+def test_curved_midsize_vs_oracle_and_errors():
+    cells, p, nq, amp = (9, 7, 6), 5, 6, 0.1
+    m, h, plan = host_tables(cells, p, deform=amp)
+    prob = oracle_problem(m, h, p, nq, geometry="curved")
+    u = np.random.default_rng(8).standard_normal(h.n_dofs)
+    ref = orc.apply(prob, u)
+    for variant in ("final_tensor_load", "quadratic_compute"):
+        op = gpu_operator(m, h, plan, p, nq, variant=variant)
+        assert rel(op.apply(u), ref) < 1e-12
+    assert op.info()["geometry_bytes"] > 0
+    with pytest.raises(ValueError):            # affine on a deformed mesh (mesh.py:214-216)
+        gpu_operator(m, h, plan, p, nq, variant="affine")
+    with pytest.raises(NotImplementedError):   # n_q > p+1 on curved meshes is outside the GPU path
+        gpu_operator(m, h, plan, p, nq + 1, variant="final_tensor_load")
+    # undeformed mesh: final-tensor variant == affine (reference tests/test_operator.py:90-95)
+    m0, h0, plan0 = host_tables((5, 4, 3), 3)
+    u0 = np.random.default_rng(9).standard_normal(h0.n_dofs)
+    a = gpu_operator(m0, h0, plan0, 3, 4).apply(u0)
+    f = gpu_operator(m0, h0, plan0, 3, 4, variant="final_tensor_load").apply(u0)
+    assert rel(f, a) < 1e-12
