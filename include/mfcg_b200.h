@@ -90,8 +90,9 @@ typedef struct mfcg_op_desc {
   int32_t precision;              /* 0 = fp64 (reference), 1 = fp32 vectors + operator    */
   int32_t brick[3];               /* cells per thread-block brick; 0 = library default    */
   /* z-slab decomposition; single GPU: slab_cells_z = cells[2], offset 0 */
-  int32_t slab_z0;                /* first global cell layer of this rank                 */
-  int32_t global_cells_z;         /* cell layers of the whole mesh                        */
+  int32_t slab_z0;                /* first global cell layer of this slab                 */
+  int32_t global_cells_z;         /* cell layers of the whole mesh (0: cells[2]); with    */
+                                  /* slabs, `cells` is the slab and `extents` the mesh    */
 } mfcg_op_desc;
 
 int mfcg_op_create(mfcg_ctx* ctx, const mfcg_op_desc* desc, mfcg_op** op);
@@ -164,6 +165,15 @@ int mfcg_solve(mfcg_op* op, const mfcg_solve_args* args, mfcg_solve_result* resu
  * communicator is set.  unique_id is the 128-byte ncclUniqueId from rank 0. */
 int mfcg_comm_unique_id(void* unique_id_128);
 int mfcg_ctx_init_comm(mfcg_ctx* ctx, const void* unique_id_128, int rank, int n_ranks);
+
+/* Slab groups: `ops` are adjacent z-slabs held by this process (bottom to top, one context).
+ * Neighbours inside the group exchange the shared lattice plane by device-to-device copies,
+ * the slabs below / above the group by ncclSend/ncclRecv with ranks rank-1 / rank+1; the seven
+ * sums of a merged iteration are reduced over the group and with one ncclAllReduce over ranks.
+ * One process per GPU uses n_ops == 1.  (No reference counterpart.) */
+int mfcg_apply_group(mfcg_op** ops, int n_ops, const double* const* src, double* const* dst, int location);
+int mfcg_diagonal_group(mfcg_op** ops, int n_ops, double* const* inv_diag, int location);
+int mfcg_solve_group(mfcg_op** ops, int n_ops, const mfcg_solve_args* args, mfcg_solve_result* results);
 
 #ifdef __cplusplus
 }

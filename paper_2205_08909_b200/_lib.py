@@ -71,7 +71,8 @@ EXPORTS = (
     "mfcg_ctx_create", "mfcg_ctx_destroy", "mfcg_ctx_stream", "mfcg_last_error", "mfcg_op_create",
     "mfcg_op_destroy", "mfcg_op_get_info", "mfcg_op_device_permutation",
     "mfcg_op_apply", "mfcg_op_diagonal", "mfcg_op_geometry", "mfcg_solve",
-    "mfcg_comm_unique_id", "mfcg_ctx_init_comm",
+    "mfcg_comm_unique_id", "mfcg_ctx_init_comm", "mfcg_apply_group", "mfcg_diagonal_group",
+    "mfcg_solve_group",
 )
 
 _lib = None
@@ -105,6 +106,9 @@ def load():
     lib.mfcg_solve.argtypes = [vp, C.POINTER(SolveArgs), C.POINTER(SolveResultC)]
     lib.mfcg_comm_unique_id.argtypes = [vp]
     lib.mfcg_ctx_init_comm.argtypes = [vp, vp, C.c_int, C.c_int]
+    lib.mfcg_apply_group.argtypes = [C.POINTER(vp), C.c_int, C.POINTER(vp), C.POINTER(vp), C.c_int]
+    lib.mfcg_diagonal_group.argtypes = [C.POINTER(vp), C.c_int, C.POINTER(vp), C.c_int]
+    lib.mfcg_solve_group.argtypes = [C.POINTER(vp), C.c_int, C.POINTER(SolveArgs), C.POINTER(SolveResultC)]
     _lib = lib
     return lib
 

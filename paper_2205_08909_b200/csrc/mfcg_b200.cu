@@ -1,6 +1,8 @@
 // mfcg_b200.cu -- C ABI (include/mfcg_b200.h) and the degree-independent host
 // logic: context, brick numbering, permutation between the caller's numbering
 // and the brick numbering, constraint mask.
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <new>
 
@@ -42,6 +44,60 @@ static const int kBrickY[2][9] = {{0, 16, 10, 6, 5, 4, 3, 2, 2}, {0, 16, 10, 6, 
 
 }  // namespace mfcg
 
+// ---------------------------------------------------------------------------
+// NCCL, bound at run time (the process already holds torch's libnccl.so.2; no link-time
+// dependency, and single-GPU use never touches it).
+namespace {
+struct NcclId { char internal[128]; };
+struct NcclApi {
+  void* lib = nullptr;
+  int (*GetUniqueId)(NcclId*) = nullptr;
+  int (*CommInitRank)(void**, int, NcclId, int) = nullptr;
+  int (*CommDestroy)(void*) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
+  int (*Send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*Recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+};
+NcclApi g_nccl;
+bool nccl_load() {
+  if (g_nccl.lib) return true;
+  const char* names[] = {"libnccl.so.2", "libnccl.so"};
+  for (const char* nm : names) {
+    g_nccl.lib = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+    if (g_nccl.lib) break;
+  }
+  if (!g_nccl.lib) { mfcg::set_error(std::string("cannot load libnccl: ") + dlerror()); return false; }
+#define MFCG_SYM(field, name) \
+  *(void**)(&g_nccl.field) = dlsym(g_nccl.lib, name); \
+  if (!g_nccl.field) { mfcg::set_error(std::string("libnccl lacks ") + name); g_nccl.lib = nullptr; return false; }
+  MFCG_SYM(GetUniqueId, "ncclGetUniqueId")
+  MFCG_SYM(CommInitRank, "ncclCommInitRank")
+  MFCG_SYM(CommDestroy, "ncclCommDestroy")
+  MFCG_SYM(GroupStart, "ncclGroupStart")
+  MFCG_SYM(GroupEnd, "ncclGroupEnd")
+  MFCG_SYM(Send, "ncclSend")
+  MFCG_SYM(Recv, "ncclRecv")
+  MFCG_SYM(AllReduce, "ncclAllReduce")
+  MFCG_SYM(GetErrorString, "ncclGetErrorString")
+#undef MFCG_SYM
+  return true;
+}
+void nccl_destroy(void* comm) { if (g_nccl.lib && comm) g_nccl.CommDestroy(comm); }
+const int kNcclUint8 = 1, kNcclFloat64 = 8, kNcclSum = 0;  // nccl.h: ncclUint8, ncclFloat64, ncclSum
+}  // namespace
+
+#define MFCG_NCCL(call)                                                                   \
+  do {                                                                                    \
+    int rc__ = (call);                                                                    \
+    if (rc__ != 0) {                                                                      \
+      mfcg::set_error(std::string(#call) + ": " + g_nccl.GetErrorString(rc__));          \
+      return MFCG_ECUDA;                                                                  \
+    }                                                                                     \
+  } while (0)
+
 using namespace mfcg;
 
 struct mfcg_ctx {
@@ -79,6 +135,7 @@ int mfcg_ctx_create(int device, mfcg_ctx** out) {
   ctx->c.device = device;
   ctx->c.sm_count = prop.multiProcessorCount;
   MFCG_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
+  MFCG_CUDA(cudaStreamCreateWithFlags(&ctx->c.comm_stream, cudaStreamNonBlocking));
   *out = ctx;
   return MFCG_OK;
 }
@@ -87,7 +144,9 @@ void* mfcg_ctx_stream(mfcg_ctx* ctx) { return ctx ? (void*)ctx->c.stream : nullp
 
 void mfcg_ctx_destroy(mfcg_ctx* ctx) {
   if (!ctx) return;
+  if (ctx->c.nccl_comm) nccl_destroy(ctx->c.nccl_comm);
   if (ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
+  if (ctx->c.comm_stream) cudaStreamDestroy(ctx->c.comm_stream);
   delete ctx;
 }
 
@@ -152,10 +211,16 @@ static int op_create_impl(mfcg_ctx* ctx, const mfcg_op_desc* d, mfcg_op* op) {
   BrickGrid& g = c.grid;
   g.p = p;
   g.n_dofs = d->n_dofs;
+  // z-slab: `cells` are this slab's cells, `extents` those of the whole mesh
+  c.global_cells_z = d->global_cells_z > 0 ? d->global_cells_z : d->cells[2];
+  c.slab_z0 = d->slab_z0;
+  if (c.slab_z0 < 0 || c.slab_z0 + d->cells[2] > c.global_cells_z) { set_error("slab layers outside the mesh"); return MFCG_EINVAL; }
+  c.has_lower = c.slab_z0 > 0;
+  c.has_upper = c.slab_z0 + d->cells[2] < c.global_cells_z;
   for (int k = 0; k < 3; ++k) {
     g.cells[k] = d->cells[k];
     c.extents[k] = d->extents[k];
-    c.h[k] = d->extents[k] / d->cells[k];
+    c.h[k] = d->extents[k] / (k == 2 ? c.global_cells_z : d->cells[k]);
   }
   // brick extents: x, y bounded by the kernel's shared-memory window; z free
   for (int k = 0; k < 2; ++k) {
@@ -257,6 +322,10 @@ static int op_create_impl(mfcg_ctx* ctx, const mfcg_op_desc* d, mfcg_op* op) {
       return MFCG_EUNSUPPORTED;
     }
   }
+  if (c.has_lower) {  // the bottom plane is a ghost copy of the lower slab's top plane
+    k_mark_ghost_plane<<<vgrid, 256, 0, st>>>(g, 0, c.d_mask);
+    MFCG_CUDA(cudaGetLastError());
+  }
   int est = MFCG_ECUDA;
   op->engine = make_engine(&c, &est);
   if (!op->engine) return est == MFCG_OK ? MFCG_ECUDA : est;
@@ -318,15 +387,227 @@ int mfcg_solve(mfcg_op* op, const mfcg_solve_args* args, mfcg_solve_result* resu
 }
 
 int mfcg_comm_unique_id(void* unique_id_128) {
-  (void)unique_id_128;
-  set_error("slab communication is not built yet in this round");
-  return MFCG_EUNSUPPORTED;
+  if (!unique_id_128) { set_error("NULL argument"); return MFCG_EINVAL; }
+  if (!nccl_load()) return MFCG_EUNSUPPORTED;
+  MFCG_NCCL(g_nccl.GetUniqueId(reinterpret_cast<NcclId*>(unique_id_128)));
+  return MFCG_OK;
 }
 
 int mfcg_ctx_init_comm(mfcg_ctx* ctx, const void* unique_id_128, int rank, int n_ranks) {
-  (void)ctx; (void)unique_id_128; (void)rank; (void)n_ranks;
-  set_error("slab communication is not built yet in this round");
-  return MFCG_EUNSUPPORTED;
+  if (!ctx || !unique_id_128 || rank < 0 || rank >= n_ranks) { set_error("bad communicator arguments"); return MFCG_EINVAL; }
+  if (!nccl_load()) return MFCG_EUNSUPPORTED;
+  cudaSetDevice(ctx->c.device);
+  NcclId id;
+  std::memcpy(&id, unique_id_128, sizeof(id));
+  MFCG_NCCL(g_nccl.CommInitRank(&ctx->c.nccl_comm, n_ranks, id, rank));
+  ctx->c.rank = rank;
+  ctx->c.n_ranks = n_ranks;
+  return MFCG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Slab groups.  `ops` are the slabs this process holds, bottom to top, all on one context.  A
+// neighbour inside the group is reached with device-to-device copies; the slab below the first
+// and above the last op belong to ranks rank-1 / rank+1 of the context's NCCL communicator.
+
+static int group_check(mfcg_op** ops, int n) {
+  if (!ops || n < 1) { set_error("empty slab group"); return MFCG_EINVAL; }
+  for (int i = 0; i < n; ++i) {
+    if (!ops[i]) { set_error("NULL operator in slab group"); return MFCG_EINVAL; }
+    if (ops[i]->common.ctx != ops[0]->common.ctx) { set_error("all slabs of a group must share one context"); return MFCG_EINVAL; }
+    if (i > 0 && !(ops[i - 1]->common.has_upper && ops[i]->common.has_lower &&
+                   ops[i - 1]->common.slab_z0 + ops[i - 1]->common.grid.cells[2] == ops[i]->common.slab_z0)) {
+      set_error("slabs of a group must be adjacent, bottom to top");
+      return MFCG_EINVAL;
+    }
+  }
+  Ctx* c = ops[0]->common.ctx;
+  if ((ops[0]->common.has_lower || ops[n - 1]->common.has_upper) && !c->nccl_comm) {
+    set_error("the group has remote neighbours but the context has no communicator (mfcg_ctx_init_comm)");
+    return MFCG_EINVAL;
+  }
+  return MFCG_OK;
+}
+
+// exchange the packed interface planes (already enqueued on the communication stream)
+static int group_exchange(mfcg_op** ops, int n, bool diag_planes) {
+  Ctx* c = ops[0]->common.ctx;
+  cudaStream_t cs = c->comm_stream;
+  for (int i = 0; i + 1 < n; ++i) {
+    const size_t bytes = ops[i]->engine->g_plane_bytes(diag_planes);
+    MFCG_CUDA(cudaMemcpyAsync(ops[i + 1]->engine->g_plane(0, 1), ops[i]->engine->g_plane(1, 0), bytes, cudaMemcpyDeviceToDevice, cs));
+    MFCG_CUDA(cudaMemcpyAsync(ops[i]->engine->g_plane(1, 1), ops[i + 1]->engine->g_plane(0, 0), bytes, cudaMemcpyDeviceToDevice, cs));
+  }
+  const bool lo = ops[0]->common.has_lower, hi = ops[n - 1]->common.has_upper;
+  if (lo || hi) {
+    MFCG_NCCL(g_nccl.GroupStart());
+    if (lo) {
+      const size_t bytes = ops[0]->engine->g_plane_bytes(diag_planes);
+      MFCG_NCCL(g_nccl.Send(ops[0]->engine->g_plane(0, 0), bytes, kNcclUint8, c->rank - 1, c->nccl_comm, cs));
+      MFCG_NCCL(g_nccl.Recv(ops[0]->engine->g_plane(0, 1), bytes, kNcclUint8, c->rank - 1, c->nccl_comm, cs));
+    }
+    if (hi) {
+      const size_t bytes = ops[n - 1]->engine->g_plane_bytes(diag_planes);
+      MFCG_NCCL(g_nccl.Send(ops[n - 1]->engine->g_plane(1, 0), bytes, kNcclUint8, c->rank + 1, c->nccl_comm, cs));
+      MFCG_NCCL(g_nccl.Recv(ops[n - 1]->engine->g_plane(1, 1), bytes, kNcclUint8, c->rank + 1, c->nccl_comm, cs));
+    }
+    MFCG_NCCL(g_nccl.GroupEnd());
+  }
+  return MFCG_OK;
+}
+
+// front halves are enqueued; exchange + unpack on the communication stream, then the compute
+// stream waits for it
+static int group_finish_exchange(mfcg_op** ops, int n, bool diag_planes, cudaEvent_t ev) {
+  Ctx* c = ops[0]->common.ctx;
+  int rc = group_exchange(ops, n, diag_planes);
+  if (rc) return rc;
+  for (int i = 0; i < n; ++i)
+    if ((rc = ops[i]->engine->g_unpack(diag_planes))) return rc;
+  MFCG_CUDA(cudaEventRecord(ev, c->comm_stream));
+  MFCG_CUDA(cudaStreamWaitEvent(c->stream, ev, 0));
+  return MFCG_OK;
+}
+
+// sums over the group's slabs (device), then over the ranks
+static __global__ void k_add_sums(double* __restrict__ acc, const double* __restrict__ x, int n, int first) {
+  if (threadIdx.x < n) acc[threadIdx.x] = first ? x[threadIdx.x] : acc[threadIdx.x] + x[threadIdx.x];
+}
+static int group_sums(mfcg_op** ops, int n, int count, double* d_global) {
+  Ctx* c = ops[0]->common.ctx;
+  for (int i = 0; i < n; ++i) k_add_sums<<<1, 32, 0, c->stream>>>(d_global, ops[i]->engine->g_sums(), count, i == 0);
+  MFCG_CUDA(cudaGetLastError());
+  if (c->nccl_comm && c->n_ranks > 1)
+    MFCG_NCCL(g_nccl.AllReduce(d_global, d_global, (size_t)count, kNcclFloat64, kNcclSum, c->nccl_comm, c->stream));
+  return MFCG_OK;
+}
+
+struct GroupScratch {
+  double* d_global = nullptr;
+  cudaEvent_t ev = nullptr;
+  ~GroupScratch() {
+    if (d_global) cudaFree(d_global);
+    if (ev) cudaEventDestroy(ev);
+  }
+  int init() {
+    MFCG_CUDA(cudaMalloc(&d_global, sizeof(double) * 8));
+    MFCG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    return MFCG_OK;
+  }
+};
+
+static int group_diagonal(mfcg_op** ops, int n, GroupScratch& gs) {
+  bool all = true;
+  for (int i = 0; i < n; ++i) all = all && ops[i]->engine->g_has_diag();
+  if (all) return MFCG_OK;
+  int rc;
+  for (int i = 0; i < n; ++i) {
+    if ((rc = ops[i]->engine->g_alloc())) return rc;
+    if ((rc = ops[i]->engine->g_diag_local())) return rc;
+    if ((rc = ops[i]->engine->g_front(true))) return rc;
+  }
+  if ((rc = group_finish_exchange(ops, n, true, gs.ev))) return rc;
+  for (int i = 0; i < n; ++i)
+    if ((rc = ops[i]->engine->g_diag_finish())) return rc;
+  return MFCG_OK;
+}
+
+int mfcg_apply_group(mfcg_op** ops, int n_ops, const double* const* src, double* const* dst, int location) {
+  int rc = group_check(ops, n_ops);
+  if (rc) return rc;
+  cudaSetDevice(ops[0]->common.ctx->device);
+  GroupScratch gs;
+  if ((rc = gs.init())) return rc;
+  for (int i = 0; i < n_ops; ++i)
+    if ((rc = ops[i]->engine->g_apply_front(src[i], location))) return rc;
+  if ((rc = group_finish_exchange(ops, n_ops, false, gs.ev))) return rc;
+  for (int i = 0; i < n_ops; ++i)
+    if ((rc = ops[i]->engine->g_apply_end(dst[i], location))) return rc;
+  return MFCG_OK;
+}
+
+int mfcg_diagonal_group(mfcg_op** ops, int n_ops, double* const* inv_diag, int location) {
+  int rc = group_check(ops, n_ops);
+  if (rc) return rc;
+  cudaSetDevice(ops[0]->common.ctx->device);
+  GroupScratch gs;
+  if ((rc = gs.init())) return rc;
+  if ((rc = group_diagonal(ops, n_ops, gs))) return rc;
+  for (int i = 0; i < n_ops; ++i)
+    if ((rc = ops[i]->engine->diagonal(inv_diag[i], location))) return rc;
+  return MFCG_OK;
+}
+
+int mfcg_solve_group(mfcg_op** ops, int n_ops, const mfcg_solve_args* args, mfcg_solve_result* results) {
+  int rc = group_check(ops, n_ops);
+  if (rc) return rc;
+  if (!args || !results) { set_error("NULL argument"); return MFCG_EINVAL; }
+  Ctx* c = ops[0]->common.ctx;
+  cudaSetDevice(c->device);
+  const mfcg_solve_args& a0 = args[0];
+  if (a0.variant != MFCG_COMBINED_PCG && a0.variant != MFCG_COMBINED_CG) {
+    set_error("slab groups run the merged variants (combined_cg / combined_pcg)");
+    return MFCG_EUNSUPPORTED;
+  }
+  if (a0.tolerance <= 0 || a0.max_iterations < 1) { set_error("bad tolerance / max_iterations"); return MFCG_EINVAL; }
+  const bool fixed = a0.fixed_iterations >= 0;
+  const int limit = a0.fixed_iterations > 0 ? a0.fixed_iterations : a0.max_iterations;
+  GroupScratch gs;
+  if ((rc = gs.init())) return rc;
+  if (a0.variant == MFCG_COMBINED_PCG && !a0.inv_diag)
+    if ((rc = group_diagonal(ops, n_ops, gs))) return rc;
+  cudaEvent_t t0, t1;
+  MFCG_CUDA(cudaEventCreate(&t0));
+  MFCG_CUDA(cudaEventCreate(&t1));
+  MFCG_CUDA(cudaEventRecord(t0, c->stream));
+  for (int i = 0; i < n_ops; ++i)
+    if ((rc = ops[i]->engine->g_begin(&args[i], limit))) return rc;
+  if ((rc = group_sums(ops, n_ops, 1, gs.d_global))) return rc;
+  double bb = 0.0;
+  MFCG_CUDA(cudaMemcpyAsync(&bb, gs.d_global, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  MFCG_CUDA(cudaStreamSynchronize(c->stream));
+  int done_iters = 0;
+  if (bb > 0.0) {
+    for (int i = 0; i < n_ops; ++i)
+      if ((rc = ops[i]->engine->g_set_state(&args[i], limit, gs.d_global))) return rc;
+    for (int it = 1; it <= limit; ++it) {
+      for (int i = 0; i < n_ops; ++i)
+        if ((rc = ops[i]->engine->g_front(false))) return rc;
+      if ((rc = group_finish_exchange(ops, n_ops, false, gs.ev))) return rc;
+      for (int i = 0; i < n_ops; ++i)
+        if ((rc = ops[i]->engine->g_post())) return rc;
+      if ((rc = group_sums(ops, n_ops, 7, gs.d_global))) return rc;
+      for (int i = 0; i < n_ops; ++i)
+        if ((rc = ops[i]->engine->g_scalar(gs.d_global))) return rc;
+      done_iters = it;
+      if (!fixed && (it % 16 == 0)) {
+        int active = 1;
+        if ((rc = ops[0]->engine->g_poll(&active))) return rc;
+        if (!active) break;
+      }
+    }
+  } else {
+    // zero right-hand side: x = 0, 0 iterations (solvers.py:156-157); the state stays zeroed
+    for (int i = 0; i < n_ops; ++i)
+      if ((rc = ops[i]->engine->g_set_state(&args[i], 0, gs.d_global))) return rc;
+  }
+  (void)done_iters;
+  int status = MFCG_OK;
+  for (int i = 0; i < n_ops; ++i) {
+    rc = ops[i]->engine->g_end(&args[i], &results[i]);
+    if (rc) status = rc;
+  }
+  MFCG_CUDA(cudaEventRecord(t1, c->stream));
+  MFCG_CUDA(cudaStreamSynchronize(c->stream));
+  float ms = 0.f;
+  MFCG_CUDA(cudaEventElapsedTime(&ms, t0, t1));
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  for (int i = 0; i < n_ops; ++i) {
+    results[i].solve_ms = ms;
+    if (bb == 0.0) results[i].converged = 1;
+  }
+  return status;
 }
 
 }  // extern "C"

@@ -28,6 +28,7 @@ struct Ctx {
   int device = 0;
   int sm_count = 148;
   cudaStream_t stream = nullptr;
+  cudaStream_t comm_stream = nullptr;  // plane exchange, overlapped with interior bricks
   void* nccl_comm = nullptr;
   int rank = 0, n_ranks = 1;
 };
@@ -41,6 +42,8 @@ struct OpCommon {
   std::vector<double> S, D, xq, wq, glx, glw, glD;
   double extents[3] = {1, 1, 1}, h[3] = {1, 1, 1}, deformation = 0.0;
   i64 n_bricks = 0;
+  int slab_z0 = 0, global_cells_z = 0;
+  bool has_lower = false, has_upper = false;  // neighbouring slabs below / above
   int* d_perm = nullptr;
   i64* d_ent_start = nullptr;
   unsigned char* d_mask = nullptr;
@@ -58,6 +61,24 @@ struct EngineBase {
   virtual int solve(const mfcg_solve_args* a, mfcg_solve_result* r) = 0;
   virtual void info(mfcg_op_info* out) = 0;
   virtual int geometry(int kind, double* out_host, i64 n_doubles) = 0;
+  // ---- slab-group driver interface (mfcg_solve_group, mfcg_b200.cu)
+  virtual int g_alloc() = 0;
+  virtual bool g_has_diag() = 0;
+  virtual int g_diag_local() = 0;
+  virtual int g_diag_finish() = 0;
+  virtual int g_begin(const mfcg_solve_args* a, int limit) = 0;
+  virtual int g_set_state(const mfcg_solve_args* a, int limit, const double* global_bb_dev) = 0;
+  virtual int g_front(bool diag_planes) = 0;
+  virtual int g_unpack(bool diag_planes) = 0;
+  virtual int g_post() = 0;
+  virtual int g_scalar(const double* global_sums_dev) = 0;
+  virtual int g_poll(int* active) = 0;
+  virtual int g_end(const mfcg_solve_args* a, mfcg_solve_result* r) = 0;
+  virtual void* g_plane(int side, int recv) = 0;
+  virtual size_t g_plane_bytes(bool diag_planes) = 0;
+  virtual double* g_sums() = 0;
+  virtual int g_apply_front(const double* src, int location) = 0;
+  virtual int g_apply_end(double* dst, int location) = 0;
 };
 
 template <int P, typename T>
@@ -75,6 +96,10 @@ class Engine : public EngineBase {
     if (d_history_) cudaFree(d_history_);
     if (geo_a_) cudaFree(geo_a_);
     if (geo_b_) cudaFree(geo_b_);
+    for (void** b : {&plane_[0][0], &plane_[0][1], &plane_[1][0], &plane_[1][1]}) if (*b) cudaFree(*b);
+    if (d_sums_) cudaFree(d_sums_);
+    if (diag_raw_) cudaFree(diag_raw_);
+    if (ev_front_) cudaEventDestroy(ev_front_);
     for (cudaEvent_t e : events_) cudaEventDestroy(e);
   }
 
@@ -207,11 +232,9 @@ class Engine : public EngineBase {
     return MFCG_OK;
   }
 
-  int ensure_diagonal() {
-    if (c_->d_invdiag) return MFCG_OK;
+  // local assembly of the (uninverted) diagonal into diag (brick numbering, fp64)
+  int assemble_diagonal(double* diag) {
     const i64 n = c_->grid.n_dofs;
-    double* diag = nullptr;
-    MFCG_CUDA(cudaMalloc(&diag, sizeof(double) * n));
     MFCG_CUDA(cudaMemsetAsync(diag, 0, sizeof(double) * n, stream()));
     MFCG_CUDA(cudaMemsetAsync(c_->d_flag, 0, sizeof(int), stream()));
     if (!general_) {
@@ -238,24 +261,35 @@ class Engine : public EngineBase {
     int gflag = 0;
     MFCG_CUDA(cudaMemcpyAsync(&gflag, c_->d_flag, sizeof(int), cudaMemcpyDeviceToHost, stream()));
     MFCG_CUDA(cudaStreamSynchronize(stream()));
-    if (gflag) {
-      cudaFree(diag);
-      set_error("degenerate cell: det J <= 0");
-      return MFCG_EINVAL;
-    }
+    if (gflag) { set_error("degenerate cell: det J <= 0"); return MFCG_EINVAL; }
+    return MFCG_OK;
+  }
+
+  // diag -> 1/diag (constrained entries 1); takes ownership of diag on success
+  int invert_diagonal(double* diag) {
     MFCG_CUDA(cudaMemsetAsync(c_->d_flag, 0, sizeof(int), stream()));
     k_diag_invert<<<vgrid_, VT, 0, stream()>>>(c_->grid, diag, c_->d_flag);
     MFCG_CUDA(cudaGetLastError());
     int flag = 0;
     MFCG_CUDA(cudaMemcpyAsync(&flag, c_->d_flag, sizeof(int), cudaMemcpyDeviceToHost, stream()));
     MFCG_CUDA(cudaStreamSynchronize(stream()));
-    if (flag) {
-      cudaFree(diag);
-      set_error("operator diagonal is not positive definite");
-      return MFCG_EINVAL;
-    }
+    if (flag) { set_error("operator diagonal is not positive definite"); return MFCG_EINVAL; }
     c_->d_invdiag = diag;
     return MFCG_OK;
+  }
+
+  int ensure_diagonal() {
+    if (c_->d_invdiag) return MFCG_OK;
+    if (c_->has_lower || c_->has_upper) {
+      set_error("a slab operator needs its neighbours for the diagonal: use the slab-group entry points");
+      return MFCG_EINVAL;
+    }
+    double* diag = nullptr;
+    MFCG_CUDA(cudaMalloc(&diag, sizeof(double) * c_->grid.n_dofs));
+    int rc = assemble_diagonal(diag);
+    if (!rc) rc = invert_diagonal(diag);
+    if (rc) cudaFree(diag);
+    return rc;
   }
 
   // caller numbering (fp64, host or device) -> brick numbering (T, device)
@@ -282,7 +316,9 @@ class Engine : public EngineBase {
     return MFCG_OK;
   }
 
-  int launch_brick(int mode, const T* src, T* pv, T* v, double* partials) {
+  int launch_brick(int mode, const T* src, T* pv, T* v, double* partials, i64 first = 0, i64 count = -1) {
+    if (count < 0) count = c_->n_bricks - first;
+    if (count == 0) return MFCG_OK;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (time_kernels_) {
       if (event_cursor_ + 2 > events_.size())
@@ -295,21 +331,22 @@ class Engine : public EngineBase {
       e1 = events_[event_cursor_++];
       MFCG_CUDA(cudaEventRecord(e0, stream()));
     }
-    const unsigned nb = (unsigned)c_->n_bricks;
+    const unsigned nb = (unsigned)count;
+    const int off = (int)first;
     if (!general_) {
       if (mode == 0)
         k_brick<P, T, 0, 0><<<nb, Cfg<P, 0>::THREADS, smem_, stream()>>>(
-            c_->grid, tab_, gen_, geo_, src, nullptr, v, nullptr, nullptr, nullptr, nullptr, nullptr);
+            c_->grid, tab_, gen_, geo_, src, nullptr, v, nullptr, nullptr, nullptr, nullptr, nullptr, off);
       else
         k_brick<P, T, 1, 0><<<nb, Cfg<P, 0>::THREADS, smem_, stream()>>>(
-            c_->grid, tab_, gen_, geo_, nullptr, pv, v, r_, x_, minv_, c_->d_state, partials);
+            c_->grid, tab_, gen_, geo_, nullptr, pv, v, r_, x_, minv_, c_->d_state, partials, off);
     } else {
       if (mode == 0)
         k_brick<P, T, 0, 1><<<nb, Cfg<P, 1>::THREADS, smem_, stream()>>>(
-            c_->grid, tab_, gen_, geo_, src, nullptr, v, nullptr, nullptr, nullptr, nullptr, nullptr);
+            c_->grid, tab_, gen_, geo_, src, nullptr, v, nullptr, nullptr, nullptr, nullptr, nullptr, off);
       else
         k_brick<P, T, 1, 1><<<nb, Cfg<P, 1>::THREADS, smem_, stream()>>>(
-            c_->grid, tab_, gen_, geo_, nullptr, pv, v, r_, x_, minv_, c_->d_state, partials);
+            c_->grid, tab_, gen_, geo_, nullptr, pv, v, r_, x_, minv_, c_->d_state, partials, off);
     }
     MFCG_CUDA(cudaGetLastError());
     if (time_kernels_) MFCG_CUDA(cudaEventRecord(e1, stream()));
@@ -336,9 +373,259 @@ class Engine : public EngineBase {
     return MFCG_OK;
   }
 
+  // ------------------------------------------------------------------ slab group interface
+ public:
+  int g_alloc() override {
+    const i64 nxy = (i64)(c_->grid.cells[0] * P + 1) * (c_->grid.cells[1] * P + 1);
+    for (int side = 0; side < 2; ++side)
+      for (int rv = 0; rv < 2; ++rv)
+        if (!plane_[side][rv]) MFCG_CUDA(cudaMalloc(&plane_[side][rv], sizeof(double) * nxy));
+    if (!d_sums_) MFCG_CUDA(cudaMalloc(&d_sums_, sizeof(double) * 8));
+    if (!ev_front_) MFCG_CUDA(cudaEventCreateWithFlags(&ev_front_, cudaEventDisableTiming));
+    return ensure_vectors(true);
+  }
+  bool g_has_diag() override { return c_->d_invdiag != nullptr; }
+  void* g_plane(int side, int recv) override { return plane_[side][recv]; }
+  size_t g_plane_bytes(bool diag_planes) override {
+    const size_t nxy = (size_t)(c_->grid.cells[0] * P + 1) * (c_->grid.cells[1] * P + 1);
+    return nxy * (diag_planes ? sizeof(double) : sizeof(T));
+  }
+  double* g_sums() override { return d_sums_; }
+
+  int g_diag_local() override {
+    if (!diag_raw_) MFCG_CUDA(cudaMalloc(&diag_raw_, sizeof(double) * c_->grid.n_dofs));
+    return assemble_diagonal(diag_raw_);
+  }
+  int g_diag_finish() override {
+    double* d = diag_raw_;
+    diag_raw_ = nullptr;
+    int rc = invert_diagonal(d);
+    if (rc) cudaFree(d);
+    return rc;
+  }
+
+  // dst = A src on a slab: everything up to the hand-over of the interface planes
+  int g_apply_front(const double* src, int location) override {
+    int rc = g_alloc();
+    if (rc) return rc;
+    if ((rc = load_vec(src, location, p_))) return rc;
+    const BrickGrid& g = c_->grid;
+    const i64 nb = c_->n_bricks, nxy = (i64)g.mb[0] * g.mb[1];
+    if (g.n_dofs > g.n_int) {
+      k_surface_init<T><<<vgrid_, VT, 0, stream()>>>(g, v_);
+      ++launches_;
+    }
+    if (g.mb[2] <= 2) {
+      if ((rc = launch_brick(0, p_, nullptr, v_, nullptr))) return rc;
+      MFCG_CUDA(cudaEventRecord(ev_front_, stream()));
+    } else {
+      if ((rc = launch_brick(0, p_, nullptr, v_, nullptr, 0, nxy))) return rc;
+      if ((rc = launch_brick(0, p_, nullptr, v_, nullptr, nb - nxy, nxy))) return rc;
+      MFCG_CUDA(cudaEventRecord(ev_front_, stream()));
+      if ((rc = launch_brick(0, p_, nullptr, v_, nullptr, nxy, nb - 2 * nxy))) return rc;
+    }
+    MFCG_CUDA(cudaStreamWaitEvent(c_->ctx->comm_stream, ev_front_, 0));
+    return pack_planes(false);
+  }
+  int g_apply_end(double* dst, int location) override {
+    const BrickGrid& g = c_->grid;
+    if (g.n_dofs > g.n_int) {
+      k_surface_fix<T><<<vgrid_, VT, 0, stream()>>>(g, p_, v_);
+      ++launches_;
+    }
+    int rc = store_vec(v_, dst, location);
+    if (rc) return rc;
+    MFCG_CUDA(cudaStreamSynchronize(stream()));
+    return MFCG_OK;
+  }
+
+  // pack the interface planes of v (or of the raw diagonal) on the communication stream
+  int pack_planes(bool diag_planes) {
+    cudaStream_t cs = c_->ctx->comm_stream;
+    const int Ktop = c_->grid.cells[2] * P;
+    if (c_->has_lower) {
+      if (diag_planes) k_plane_pack<double><<<vgrid_, VT, 0, cs>>>(c_->grid, 0, diag_raw_, (double*)plane_[0][0]);
+      else k_plane_pack<T><<<vgrid_, VT, 0, cs>>>(c_->grid, 0, v_, (T*)plane_[0][0]);
+      ++launches_;
+    }
+    if (c_->has_upper) {
+      if (diag_planes) k_plane_pack<double><<<vgrid_, VT, 0, cs>>>(c_->grid, Ktop, diag_raw_, (double*)plane_[1][0]);
+      else k_plane_pack<T><<<vgrid_, VT, 0, cs>>>(c_->grid, Ktop, v_, (T*)plane_[1][0]);
+      ++launches_;
+    }
+    MFCG_CUDA(cudaGetLastError());
+    return MFCG_OK;
+  }
+
+  // one merged iteration up to the hand-over of the interface planes: pre on shared DoFs, the
+  // brick layers touching the interface first, then (event) the interior layers on the compute
+  // stream while the planes are packed on the communication stream
+  int g_front(bool diag_planes) override {
+    cudaStream_t cs = c_->ctx->comm_stream;
+    if (diag_planes) {
+      MFCG_CUDA(cudaEventRecord(ev_front_, stream()));
+      MFCG_CUDA(cudaStreamWaitEvent(cs, ev_front_, 0));
+      return pack_planes(true);
+    }
+    const BrickGrid& g = c_->grid;
+    const i64 n = g.n_dofs, nb = c_->n_bricks, nxy = (i64)g.mb[0] * g.mb[1];
+    if (n > g.n_int) {
+      k_pre<T><<<vgrid_, VT, 0, stream()>>>(g, g.n_int, n, 1, r_, p_, v_, x_, minv_, c_->d_state);
+      ++launches_;
+    }
+    int rc;
+    if (g.mb[2] <= 2) {
+      if ((rc = launch_brick(1, nullptr, p_, v_, partials_a_))) return rc;
+      MFCG_CUDA(cudaEventRecord(ev_front_, stream()));
+    } else {
+      if ((rc = launch_brick(1, nullptr, p_, v_, partials_a_, 0, nxy))) return rc;
+      if ((rc = launch_brick(1, nullptr, p_, v_, partials_a_, nb - nxy, nxy))) return rc;
+      MFCG_CUDA(cudaEventRecord(ev_front_, stream()));
+      if ((rc = launch_brick(1, nullptr, p_, v_, partials_a_, nxy, nb - 2 * nxy))) return rc;
+    }
+    MFCG_CUDA(cudaStreamWaitEvent(cs, ev_front_, 0));
+    return pack_planes(false);
+  }
+
+  // add the neighbours' contributions (communication stream)
+  int g_unpack(bool diag_planes) override {
+    cudaStream_t cs = c_->ctx->comm_stream;
+    const int Ktop = c_->grid.cells[2] * P;
+    if (c_->has_lower) {
+      if (diag_planes) k_plane_add<double><<<vgrid_, VT, 0, cs>>>(c_->grid, 0, diag_raw_, (const double*)plane_[0][1]);
+      else k_plane_add<T><<<vgrid_, VT, 0, cs>>>(c_->grid, 0, v_, (const T*)plane_[0][1]);
+      ++launches_;
+    }
+    if (c_->has_upper) {
+      if (diag_planes) k_plane_add<double><<<vgrid_, VT, 0, cs>>>(c_->grid, Ktop, diag_raw_, (const double*)plane_[1][1]);
+      else k_plane_add<T><<<vgrid_, VT, 0, cs>>>(c_->grid, Ktop, v_, (const T*)plane_[1][1]);
+      ++launches_;
+    }
+    MFCG_CUDA(cudaGetLastError());
+    return MFCG_OK;
+  }
+
+  // post on the shared range (ghost plane excluded) and the slab's seven sums
+  int g_post() override {
+    const BrickGrid& g = c_->grid;
+    const i64 n = g.n_dofs;
+    int rows = (int)c_->n_bricks;
+    if (n > g.n_int) {
+      k_post<T><<<vgrid_, VT, 0, stream()>>>(g, g.n_int, n, 1, r_, p_, v_, minv_, c_->d_state,
+                                             partials_a_ + 8 * c_->n_bricks);
+      rows += vgrid_;
+      ++launches_;
+    }
+    k_reduce_partials<<<1, 256, 0, stream()>>>(partials_a_, rows, 7, 0, d_sums_);
+    ++launches_;
+    MFCG_CUDA(cudaGetLastError());
+    return MFCG_OK;
+  }
+
+  int g_scalar(const double* global_sums_dev) override {
+    k_scalar_merged_sums<<<1, 32, 0, stream()>>>(global_sums_dev, c_->d_state, d_history_);
+    ++launches_;
+    MFCG_CUDA(cudaGetLastError());
+    return MFCG_OK;
+  }
+
+  int g_poll(int* active) override {
+    MFCG_CUDA(cudaMemcpyAsync(c_->h_state, c_->d_state, sizeof(SolveState), cudaMemcpyDeviceToHost, stream()));
+    MFCG_CUDA(cudaStreamSynchronize(stream()));
+    *active = c_->h_state->active;
+    return MFCG_OK;
+  }
+
+  // right-hand side, preconditioner, zero vectors, this slab's part of b.b
+  int g_begin(const mfcg_solve_args* a, int limit) override {
+    const i64 n = c_->grid.n_dofs;
+    int rc = g_alloc();
+    if (rc) return rc;
+    if (history_cap_ < limit) {
+      if (d_history_) cudaFree(d_history_);
+      MFCG_CUDA(cudaMalloc(&d_history_, sizeof(double) * 4 * (size_t)limit));
+      history_cap_ = limit;
+    }
+    launches_ = op_launches_ = 0;
+    time_kernels_ = false;
+    event_cursor_ = 0;
+    if ((rc = load_vec(a->b, a->location, r_))) return rc;
+    const bool prec = a->variant == MFCG_COMBINED_PCG;
+    if (prec) {
+      if (a->inv_diag) {
+        if ((rc = load_vec(a->inv_diag, a->location, minv_))) return rc;
+      } else {
+        k_convert<T, double><<<vgrid_, VT, 0, stream()>>>(n, c_->d_invdiag, minv_);
+        ++launches_;
+      }
+    } else {
+      k_fill<T><<<vgrid_, VT, 0, stream()>>>(n, minv_, (T)1);
+      ++launches_;
+    }
+    MFCG_CUDA(cudaMemsetAsync(x_, 0, sizeof(T) * n, stream()));
+    MFCG_CUDA(cudaMemsetAsync(p_, 0, sizeof(T) * n, stream()));
+    MFCG_CUDA(cudaMemsetAsync(v_, 0, sizeof(T) * n, stream()));
+    k_dot_owned<T><<<vgrid_, VT, 0, stream()>>>(c_->grid, r_, r_, partials_a_);
+    k_reduce_partials<<<1, 256, 0, stream()>>>(partials_a_, vgrid_, 1, 0, d_sums_);
+    launches_ += 2;
+    MFCG_CUDA(cudaGetLastError());
+    return MFCG_OK;
+  }
+
+  int g_set_state(const mfcg_solve_args* a, int limit, const double* global_bb_dev) override {
+    SolveState s0;
+    std::memset(&s0, 0, sizeof(s0));
+    s0.active = 1;
+    s0.fixed = a->fixed_iterations >= 0 ? 1 : 0;
+    s0.force_x = a->force_x_updates ? 1 : 0;
+    s0.has_prec = a->variant == MFCG_COMBINED_PCG ? 1 : 0;
+    s0.limit = limit;
+    s0.tol = a->tolerance;
+    s0.residual = 1.0;
+    *c_->h_state = s0;
+    MFCG_CUDA(cudaMemcpyAsync(c_->d_state, c_->h_state, sizeof(SolveState), cudaMemcpyHostToDevice, stream()));
+    k_set_bnorm<<<1, 1, 0, stream()>>>(c_->d_state, global_bb_dev);
+    MFCG_CUDA(cudaGetLastError());
+    return MFCG_OK;
+  }
+
+  int g_end(const mfcg_solve_args* a, mfcg_solve_result* res) override {
+    std::memset(res, 0, sizeof(*res));
+    const i64 n = c_->grid.n_dofs;
+    k_finalize_x<T><<<vgrid_, VT, 0, stream()>>>(n, x_, p_, r_, minv_, c_->d_state);
+    ++launches_;
+    int rc = store_vec(x_, a->x, a->location);
+    if (rc) return rc;
+    MFCG_CUDA(cudaMemcpyAsync(c_->h_state, c_->d_state, sizeof(SolveState), cudaMemcpyDeviceToHost, stream()));
+    MFCG_CUDA(cudaStreamSynchronize(stream()));
+    const SolveState& s = *c_->h_state;
+    res->bnorm = s.bnorm;
+    res->kernel_launches = launches_;
+    res->operator_launches = op_launches_;
+    res->iterations = s.k;
+    res->matvecs = s.k;
+    res->residual = s.residual;
+    res->breakdown = s.breakdown;
+    res->breakdown_iteration = s.breakdown_iteration;
+    res->breakdown_value = s.breakdown_value;
+    res->converged = a->fixed_iterations >= 0 ? (s.residual < a->tolerance) : s.converged;
+    if (a->history && s.k > 0)
+      MFCG_CUDA(cudaMemcpy(a->history, d_history_, sizeof(double) * 4 * (size_t)s.k, cudaMemcpyDeviceToHost));
+    if (s.breakdown) {
+      char buf[160];
+      std::snprintf(buf, sizeof(buf), "breakdown code %d: value %.3e <= 0 at iteration %d", s.breakdown,
+                    s.breakdown_value, s.breakdown_iteration);
+      set_error(buf);
+      return MFCG_EBREAKDOWN;
+    }
+    return MFCG_OK;
+  }
+
+ private:
   GeoMesh geo_mesh() const {
     GeoMesh gm{};
     for (int d = 0; d < 3; ++d) { gm.cells[d] = c_->grid.cells[d]; gm.h[d] = c_->h[d]; gm.ext[d] = c_->extents[d]; }
+    gm.z0 = c_->slab_z0;
     gm.amp = c_->deformation;
     return gm;
   }
@@ -437,6 +724,10 @@ class Engine : public EngineBase {
   void* geo_b_ = nullptr;
   i64 geo_bytes_ = 0;
   bool general_ = false;
+  void* plane_[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [side lo/hi][send/recv]
+  double* d_sums_ = nullptr;
+  double* diag_raw_ = nullptr;  // slab runs: diagonal before the interface exchange
+  cudaEvent_t ev_front_ = nullptr;
   int smem_ = 0, vgrid_ = 0;
   T *x_ = nullptr, *r_ = nullptr, *p_ = nullptr, *v_ = nullptr, *z_ = nullptr, *minv_ = nullptr;
   double *partials_a_ = nullptr, *partials_b_ = nullptr, *d_history_ = nullptr;

@@ -54,7 +54,7 @@ struct BrickGrid {
   i64 n_dofs;
   i64 n_int;      // brick-interior DoFs occupy [0, n_int)
   const i64* ent_start;        // start of every macro entity, [2mbz+1][2mby+1][2mbx+1]
-  const unsigned char* mask;   // constrained flag of shared DoF n_int + s
+  const unsigned char* mask;   // per shared DoF n_int + s: bit 0 constrained, bit 1 ghost copy (owned by the lower slab)
 };
 
 // Device-resident solver state: the iteration loop never synchronises with
@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(Cfg<P, G>::THREADS, Cfg<P, G>::MINB)
 k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAccess geo,
         const T* __restrict__ src, T* __restrict__ Pv,
         T* __restrict__ V, T* __restrict__ R, T* __restrict__ X, const T* __restrict__ Minv,
-        const SolveState* __restrict__ st, double* __restrict__ partials) {
+        const SolveState* __restrict__ st, double* __restrict__ partials, int brick_offset) {
   constexpr int N = P + 1, RS = Geo<P, G>::RS, TILE = Geo<P, G>::TILE, WX = Geo<P, G>::WX,
                 PLANE = Geo<P, G>::PLANE, NCELL = Geo<P, G>::NCELL, RB = Geo<P, G>::RB,
                 NT_C = Cfg<P, G>::NT_C, NT_P = Cfg<P, G>::NT_P, KC = Cfg<P, G>::KC, HE = EOShape<N>::HE;
@@ -427,7 +427,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
     am1 = (T)st->am1; bm1 = (T)st->bm1; xc1 = (T)st->xc1; xc2 = (T)st->xc2; xmode = st->xmode;
   }
 
-  const int b = blockIdx.x;
+  const int b = blockIdx.x + brick_offset;  // slab runs launch the interface brick layers first
   const int mx = b % g.mb[0];
   const int my = (b / g.mb[0]) % g.mb[1];
   const int mz = b / (g.mb[0] * g.mb[1]);
@@ -566,7 +566,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
                 const int ez = K == 0 ? 0 : (K == Lz ? 2 : 1);
                 const i64 gi = st27[ex + 3 * ey + 9 * ez] + ox + lx * oy + (ez == 1 ? (i64)(lx * ly) * (K - 1) : 0);
                 pp[c] = MODE == 0 ? src[gi] : Pv[gi];
-                mk[c] = g.mask[gi - n_int];
+                mk[c] = g.mask[gi - n_int] & 1;
                 dst[c] = (K % RB) * PLANE + j * WX + i;
               }
             }
@@ -583,7 +583,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
           const int slot = ((side == 0 ? 0 : Lz) % RB) * PLANE;
           for (int it = ptid; it < nint2d; it += NT_P) {
             const T pv = MODE == 0 ? src[fb + it] : Pv[fb + it];
-            const unsigned char mk = g.mask[fb + it - n_int];
+            const unsigned char mk = g.mask[fb + it - n_int] & 1;
             const int jm = (int)(((unsigned)it * lxm_magic) >> 16);
             const int im = it - jm * lxm;
             ring[slot + (jm + 1) * WX + im + 1] = mk ? (T)0 : pv;
@@ -946,7 +946,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
     if (tid < 7) {
       double acc = 0.0;
       for (int w = 0; w < NT_P / 32; ++w) acc += red[w * 7 + tid];
-      partials[(i64)blockIdx.x * 8 + tid] = acc;
+      partials[(i64)b * 8 + tid] = acc;
     }
   }
 }
@@ -967,7 +967,7 @@ template <typename T>
 __global__ void k_surface_fix(BrickGrid g, const T* __restrict__ src, T* __restrict__ dst) {
   const i64 n_sh = g.n_dofs - g.n_int;
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n_sh; i += (i64)gridDim.x * blockDim.x)
-    if (g.mask[i]) dst[g.n_int + i] = src[g.n_int + i];
+    if (g.mask[i] & 1) dst[g.n_int + i] = src[g.n_int + i];
 }
 
 // merged-CG "pre" (solvers.py:660-690); with init_v also zeroes v for the
@@ -1007,10 +1007,12 @@ __global__ void k_post(BrickGrid g, i64 lo, i64 hi, int fix_constrained, const T
   for (i64 i = lo + blockIdx.x * (i64)blockDim.x + threadIdx.x; i < hi; i += (i64)gridDim.x * blockDim.x) {
     const double r = (double)R[i], p = (double)Pv[i], m = (double)Minv[i];
     double v = (double)V[i];
-    if (fix_constrained && i >= g.n_int && g.mask[i - g.n_int]) {  // identity row: v_c = p_c
+    unsigned char flag = i >= g.n_int ? g.mask[i - g.n_int] : (unsigned char)0;
+    if (fix_constrained && (flag & 1)) {  // identity row: v_c = p_c
       v = p;
       V[i] = (T)p;
     }
+    if (flag & 2) continue;  // ghost copy of the lower slab's plane: counted there
     const double mr = m * r, mv = m * v;
     s[0] += r * r; s[1] += p * v; s[2] += r * v; s[3] += v * v;
     s[4] += r * mr; s[5] += r * mv; s[6] += v * mv;
@@ -1053,18 +1055,8 @@ __device__ __forceinline__ void reduce_rows(const double* __restrict__ partials,
   __syncthreads();
 }
 
-// Scalar step of the merged iteration (solvers.py:706-764), one block.
-static __global__ void k_scalar_merged(const double* __restrict__ partials, int rows, SolveState* st,
-                                double* __restrict__ history) {
-  __shared__ double red[7 * 32];
-  __shared__ double sums[8];
-  if (!st->active) return;
-  reduce_rows(partials, rows, 7, sums, red);
-  if (threadIdx.x != 0) return;
-#if MFCG_SKIP
-  // timing experiments only: keep iterating on garbage
-  sums[0] = sums[1] = sums[3] = sums[4] = sums[6] = 1.0; sums[2] = sums[5] = 0.25;
-#endif
+// Scalar step of the merged iteration (solvers.py:706-764) on the seven reduced sums.
+__device__ __forceinline__ void merged_scalar_step(const double* sums, SolveState* st, double* __restrict__ history) {
   const double gamma = sums[0], a = sums[1], bb = sums[2], cc = sums[3], d = sums[4], e = sums[5], f = sums[6];
   const int k = st->k + 1;
   const bool fixed = st->fixed != 0;
@@ -1113,6 +1105,38 @@ static __global__ void k_scalar_merged(const double* __restrict__ partials, int 
     st->xc1 = st->am1;
   }
   st->xmode = xmode;
+}
+
+// one block: reduce the per-block partial rows, then the scalar step
+static __global__ void k_scalar_merged(const double* __restrict__ partials, int rows, SolveState* st,
+                                       double* __restrict__ history) {
+  __shared__ double red[7 * 32];
+  __shared__ double sums[8];
+  if (!st->active) return;
+  reduce_rows(partials, rows, 7, sums, red);
+  if (threadIdx.x != 0) return;
+#if MFCG_SKIP
+  // timing experiments only: keep iterating on garbage
+  sums[0] = sums[1] = sums[3] = sums[4] = sums[6] = 1.0; sums[2] = sums[5] = 0.25;
+#endif
+  merged_scalar_step(sums, st, history);
+}
+
+// slab runs: the sums arrive already reduced over all slabs / ranks
+static __global__ void k_scalar_merged_sums(const double* __restrict__ sums, SolveState* st,
+                                            double* __restrict__ history) {
+  if (!st->active || threadIdx.x != 0) return;
+  merged_scalar_step(sums, st, history);
+}
+
+// out[0..cols) = deterministic sum of the partial rows; acc != 0: add to out instead of overwriting
+static __global__ void k_reduce_partials(const double* __restrict__ partials, int rows, int cols, int acc,
+                                         double* __restrict__ out) {
+  __shared__ double red[7 * 32];
+  __shared__ double sums[8];
+  reduce_rows(partials, rows, cols, sums, red);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < cols; ++q) out[q] = acc ? out[q] + sums[q] : sums[q];
 }
 
 // ---------------------------------------------------------------------------
@@ -1297,9 +1321,52 @@ static __global__ void k_mark_constrained(i64 k, const i64* __restrict__ constra
   for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < k; t += (i64)gridDim.x * blockDim.x) {
     const i64 d = perm[constrained[t]];
     if (d < n_int) *error = 1;  // a constrained DoF strictly inside a brick: not a boundary constraint
-    else mask[d - n_int] = 1;
+    else mask[d - n_int] |= 1;
   }
 }
+
+// ---------------------------------------------------------------------------
+// z-slab decomposition: neighbouring slabs share one lattice plane; both hold it,
+// the lower slab owns it for the dot products.  buf[J * NX + I] <-> vector entry of lattice point
+// (I, J, K) of this slab in brick numbering.
+template <typename T>
+__global__ void k_plane_pack(BrickGrid g, int K, const T* __restrict__ vec, T* __restrict__ buf) {
+  const int NX = g.cells[0] * g.p + 1, NY = g.cells[1] * g.p + 1;
+  for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < (i64)NX * NY; t += (i64)gridDim.x * blockDim.x) {
+    const int J = (int)(t / NX), I = (int)(t - (i64)J * NX);
+    buf[t] = vec[lattice_to_dev(g, I, J, K)];
+  }
+}
+template <typename T>
+__global__ void k_plane_add(BrickGrid g, int K, T* __restrict__ vec, const T* __restrict__ buf) {
+  const int NX = g.cells[0] * g.p + 1, NY = g.cells[1] * g.p + 1;
+  for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < (i64)NX * NY; t += (i64)gridDim.x * blockDim.x) {
+    const int J = (int)(t / NX), I = (int)(t - (i64)J * NX);
+    vec[lattice_to_dev(g, I, J, K)] += buf[t];
+  }
+}
+// flag the slab's bottom plane as a ghost copy (bit 1)
+static __global__ void k_mark_ghost_plane(BrickGrid g, int K, unsigned char* __restrict__ mask) {
+  const int NX = g.cells[0] * g.p + 1, NY = g.cells[1] * g.p + 1;
+  for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < (i64)NX * NY; t += (i64)gridDim.x * blockDim.x) {
+    const int J = (int)(t / NX), I = (int)(t - (i64)J * NX);
+    mask[lattice_to_dev(g, I, J, K) - g.n_int] |= 2;
+  }
+}
+// partial sums of a.b over the DoFs this slab owns
+template <typename T>
+__global__ void k_dot_owned(BrickGrid g, const T* __restrict__ a, const T* __restrict__ b,
+                            double* __restrict__ partials) {
+  __shared__ double red[7 * 32];
+  double s[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < g.n_dofs; i += (i64)gridDim.x * blockDim.x) {
+    if (i >= g.n_int && (g.mask[i - g.n_int] & 2)) continue;
+    s[0] += (double)a[i] * (double)b[i];
+  }
+  block_reduce7_store(s, red, partials + (i64)blockIdx.x * 8);
+}
+// state for a slab run is written by the host; this sets the norm all slabs share
+static __global__ void k_set_bnorm(SolveState* st, const double* __restrict__ sums) { st->bnorm = sqrt(sums[0]); }
 
 // ---------------------------------------------------------------------------
 // Jacobi diagonal, GL collocation, affine geometry (operator.py:380-418):
@@ -1327,7 +1394,7 @@ static __global__ void k_diag_affine(BrickGrid g, DiagTables t, i64 n_cells, dou
 static __global__ void k_diag_invert(BrickGrid g, double* __restrict__ diag, int* __restrict__ error) {
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < g.n_dofs; i += (i64)gridDim.x * blockDim.x) {
     double d = diag[i];
-    if (i >= g.n_int && g.mask[i - g.n_int]) d = 1.0;
+    if (i >= g.n_int && (g.mask[i - g.n_int] & 1)) d = 1.0;
     if (!(d > 0.0) || isinf(d)) *error = 1;
     diag[i] = 1.0 / d;
   }
@@ -1351,8 +1418,9 @@ __global__ void k_fill(i64 n, T* __restrict__ out, T value) {
 // tri-quadratic nodes of the cell are the sine-bump map of the {0,1/2,1}^3 lattice
 // (mesh.py:73-80), then every thread evaluates Jacobians at tensor points.
 struct GeoMesh {
-  int cells[3];
-  double h[3], ext[3], amp;
+  int cells[3];   // cells of this slab
+  int z0;         // first global cell layer of the slab
+  double h[3], ext[3], amp;  // ext: extents of the whole mesh
 };
 struct PointTab {   // quadratic basis on {0,1/2,1} at up to 10 1D points, and their weights
   double qv[30], qd[30], w[10];
@@ -1361,7 +1429,7 @@ struct PointTab {   // quadratic basis on {0,1/2,1} at up to 10 1D points, and t
 
 __device__ __forceinline__ void cell_nodes_to_smem(const GeoMesh& gm, i64 cell, double* nodes /*[81]*/) {
   const int cx = (int)(cell % gm.cells[0]), cy = (int)((cell / gm.cells[0]) % gm.cells[1]),
-            cz = (int)(cell / ((i64)gm.cells[0] * gm.cells[1]));
+            cz = (int)(cell / ((i64)gm.cells[0] * gm.cells[1])) + gm.z0;
   const double kPi = 3.14159265358979323846;
   if (threadIdx.x < 27) {
     const int a = threadIdx.x % 3, b = (threadIdx.x / 3) % 3, c = threadIdx.x / 9;

@@ -96,7 +96,7 @@ class MatrixFreeOperator:
 
     def __init__(self, spec: OperatorSpec, mesh: HexMesh, handler: DofHandler,
                  plan: BatchPlan, *, device: int = 0, precision: str = "fp64",
-                 brick=(0, 0, 0)):
+                 brick=(0, 0, 0), slab_z0: int = 0, global_cells_z: int = None):
         if spec.components != handler.components:
             raise ValueError("spec/handler component mismatch")
         if spec.degree != handler.degree:
@@ -149,8 +149,10 @@ class MatrixFreeOperator:
             raise NotImplementedError(f"geometry variant {spec.geometry.value} is outside the hot-path scope")
         d.precision = 0 if precision == "fp64" else 1
         d.brick = (C.c_int32 * 3)(*brick)
-        d.slab_z0 = 0
-        d.global_cells_z = mesh.cells_per_dim[2]
+        # z-slab of a larger mesh (slabs.py): `mesh` is the slab, its extents those of the whole mesh
+        d.slab_z0 = int(slab_z0)
+        d.global_cells_z = int(global_cells_z) if global_cells_z else mesh.cells_per_dim[2]
+        self.slab_z0, self.global_cells_z = d.slab_z0, d.global_cells_z
         handle = C.c_void_p()
         _lib.check(self._lib.mfcg_op_create(self._ctx, C.byref(d), C.byref(handle)))
         self._handle = handle

@@ -1,0 +1,148 @@
+"""z-slab decomposition: host tables (CPU, incl. a world_size-2 gloo run) and the single-GPU
+lockstep emulation of 2-4 slabs against the one-slab operator."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2205_08909_b200 import dofs, mesh as pmesh, slabs
+from _problems import gpu_operator, hist_array, host_tables, rel, seeded_rhs
+
+
+def _global(cells, p):
+    m = pmesh.build_cartesian_mesh(cells)
+    return m, dofs.distribute_dofs(m, p, 1, constrain_boundary=True)
+
+
+def _global_lattice_of(h, p):
+    node, I, J, K = slabs._lattice_ids(h, 0)
+    nx, ny, nz = h.cells_per_dim
+    out = np.empty(h.n_dofs, dtype=np.int64)
+    out[node] = I + (nx * p + 1) * (J + (ny * p + 1) * K)
+    return out
+
+
+@pytest.mark.parametrize("cells,p,G", [((3, 2, 5), 2, 2), ((4, 3, 7), 3, 3), ((2, 2, 8), 5, 4)])
+def test_slab_tables_against_global_numbering(cells, p, G):
+    m, h = _global(cells, p)
+    lat_of_global = _global_lattice_of(h, p)           # global node -> lattice id
+    glob_of_lat = np.empty_like(lat_of_global)
+    glob_of_lat[lat_of_global] = np.arange(h.n_dofs)   # lattice id -> global node (reference numbering)
+    layers = slabs.slab_layers(cells[2], G)
+    assert sum(n for _, n in layers) == cells[2] and layers[0][0] == 0
+    sl = [slabs.build_slab(m, p, z0, n) for z0, n in layers]
+    covered = np.zeros(h.n_dofs, dtype=int)
+    for g, s in enumerate(sl):
+        gl = glob_of_lat[s.global_nodes]                # local node -> global node id
+        # numbering: the slab's block table maps onto the reference's global one, cell by cell
+        nxy = cells[0] * cells[1]
+        loc = dofs.expand_batch(s.handler, np.arange(s.handler.n_cells))
+        ref = dofs.expand_batch(h, np.arange(s.handler.n_cells) + s.z0 * nxy)
+        assert np.array_equal(gl[loc], ref)
+        # Dirichlet set = global set restricted to the slab
+        assert np.array_equal(np.sort(gl[s.handler.constrained_dofs]),
+                              np.intersect1d(h.constrained_dofs, gl))
+        covered[gl] += 1
+        # ghost map: shared plane = intersection of the two slabs' DoFs
+        if g + 1 < G:
+            up = sl[g + 1]
+            mine = gl[slabs.interface_plane_nodes(s, "upper")]
+            theirs = glob_of_lat[up.global_nodes][slabs.interface_plane_nodes(up, "lower")]
+            cells_lo = np.arange(s.handler.n_cells) + s.z0 * nxy
+            cells_up = np.arange(up.handler.n_cells) + up.z0 * nxy
+            shared = np.intersect1d(np.unique(dofs.expand_batch(h, cells_lo)),
+                                    np.unique(dofs.expand_batch(h, cells_up)))
+            assert np.array_equal(np.sort(mine), shared) and np.array_equal(mine, theirs)
+    assert covered.min() == 1 and covered.max() == 2 and (covered == 2).sum() == (G - 1) * (
+        (cells[0] * p + 1) * (cells[1] * p + 1))
+
+
+def _gloo_worker(rank, world, port, q):
+    import torch.distributed as dist
+    import torch
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cells, p = (3, 2, 6), 3
+    m = pmesh.build_cartesian_mesh(cells)
+    z0, n = slabs.slab_layers(cells[2], world)[rank]
+    s = slabs.build_slab(m, p, z0, n)
+    ok = True
+    # neighbours agree on the ghost map (global lattice ids of the shared plane, same order)
+    if s.has_upper:
+        mine = torch.from_numpy(s.global_nodes[slabs.interface_plane_nodes(s, "upper")])
+        dist.send(mine, rank + 1)
+    if s.has_lower:
+        mine = torch.from_numpy(s.global_nodes[slabs.interface_plane_nodes(s, "lower")])
+        theirs = torch.empty_like(mine)
+        dist.recv(theirs, rank - 1)
+        ok = ok and bool(torch.equal(mine, theirs))
+    # owned-DoF count and a seven-scalar all-reduce, the collective of one merged iteration
+    owned = s.handler.n_dofs - (len(interface := slabs.interface_plane_nodes(s, "lower")) if s.has_lower else 0)
+    t = torch.tensor([float(owned)] + [float(rank + 1)] * 6, dtype=torch.float64)
+    dist.all_reduce(t)
+    total = int(np.prod([c * p + 1 for c in cells]))
+    ok = ok and int(t[0]) == total and float(t[1]) == world * (world + 1) / 2
+    q.put((rank, ok))
+    dist.destroy_process_group()
+
+
+def test_slab_host_logic_world_size_2_gloo():
+    import torch.multiprocessing as mp
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    results = sorted(q.get(timeout=120) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=60)
+    assert results == [(0, True), (1, True)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cells,p,G,deform", [((5, 4, 9), 5, 2, 0.0), ((6, 5, 12), 3, 3, 0.0),
+                                              ((4, 4, 17), 5, 4, 0.0), ((4, 3, 6), 3, 2, 0.1)])
+def test_slab_group_equals_single_slab_on_one_gpu(cells, p, G, deform):
+    """G slabs stepped in lockstep on one GPU (device-to-device plane copies stand in for NCCL)
+    against the one-slab operator: apply and diagonal at 1e-12, merged-CG history at 1e-10."""
+    from paper_2205_08909_b200 import solvers as S
+    from paper_2205_08909_b200.operator import MatrixFreeOperator, OperatorSpec
+    variant = "final_tensor_load" if deform else "affine"
+    m, h, plan = host_tables(cells, p, deform=deform)
+    op1 = gpu_operator(m, h, plan, p, p + 1, variant=variant)
+    lat = _global_lattice_of(h, p)
+    glob_of_lat = np.empty_like(lat)
+    glob_of_lat[lat] = np.arange(h.n_dofs)
+    sl = [slabs.build_slab(m, p, z0, n) for z0, n in slabs.slab_layers(cells[2], G)]
+    ops = []
+    for s in sl:
+        plan_s = dofs.make_batches(s.mesh, dofs.batch_size(p, 1, 8), "morton")
+        ops.append(MatrixFreeOperator(OperatorSpec("laplace", 1, p, p + 1, pmesh.GeometryVariant(variant)),
+                                      s.mesh, s.handler, plan_s, slab_z0=s.z0,
+                                      global_cells_z=s.global_cells_z))
+    maps = [glob_of_lat[s.global_nodes] for s in sl]
+    group = slabs.SlabGroup(ops)
+    u = np.random.default_rng(3).standard_normal(h.n_dofs)
+    ref = op1.apply(u)
+    for gl, out in zip(maps, group.apply([u[gl] for gl in maps])):
+        assert rel(out, ref[gl]) < 1e-12
+    dref = op1.compute_diagonal().inverse_diagonal
+    for gl, d in zip(maps, group.compute_diagonal()):
+        assert rel(d, dref[gl]) < 1e-12
+    b = seeded_rhs(h)
+    cfg = S.SolverConfig(fixed_iterations=40)
+    one = S.solve("combined_pcg", op1, b, minv=op1.compute_diagonal(), config=cfg)
+    many = group.solve("combined_pcg", [b[gl] for gl in maps], cfg)
+    H1 = hist_array(one.history)
+    for gl, r in zip(maps, many):
+        assert r.iterations == 40
+        assert rel(hist_array(r.history)[:30], H1[:30]) < 1e-10
+        assert rel(r.x, one.x[gl]) < 1e-9
+    # tolerance-terminated run agrees on the iteration count
+    one = S.solve("combined_pcg", op1, b, minv=op1.compute_diagonal(), config=S.SolverConfig(tolerance=1e-7))
+    many = group.solve("combined_pcg", [b[gl] for gl in maps], S.SolverConfig(tolerance=1e-7))
+    assert all(abs(r.iterations - one.iterations) <= 1 and r.converged for r in many)
