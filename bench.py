@@ -203,6 +203,96 @@ def workload_config(args, n_gpus):
             "parallelism": "1 GPU" if n_gpus == 1 else f"z-slabs x{n_gpus}"}
 
 
+def run_slabs(args, rank, local_rank, world):
+    """N > 1: BASELINE configs[4] weak scaling -- 80^3 cells per GPU stacked in z, one process per
+    GPU, shared lattice planes exchanged with ncclSend/ncclRecv, seven sums per iteration through
+    one ncclAllReduce.  No data-path collective beyond those two."""
+    import torch
+    import torch.distributed as dist
+    from paper_2205_08909_b200 import _lib, dofs, mesh as pmesh, slabs
+    from paper_2205_08909_b200.operator import MatrixFreeOperator, OperatorSpec
+    from paper_2205_08909_b200.solvers import SolverConfig
+    dist.init_process_group("nccl", rank=rank, world_size=world)
+    p = args.degree
+    cells = workload_cells(args, world)
+    gmesh = pmesh.build_cartesian_mesh(cells)
+    z0, nzg = slabs.slab_layers(cells[2], world)[rank]
+    slab = slabs.build_slab(gmesh, p, z0, nzg)
+    plan = dofs.make_batches(slab.mesh, dofs.batch_size(p, 1, 8), "morton")
+    uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        uid.copy_(torch.frombuffer(bytearray(slabs.new_unique_id()), dtype=torch.uint8))
+    dist.broadcast(uid, 0)
+    slabs.init_comm(local_rank, bytes(uid.cpu().numpy().tobytes()), rank, world)
+    op = MatrixFreeOperator(OperatorSpec("laplace", 1, p, p + 1, pmesh.GeometryVariant.AFFINE), slab.mesh,
+                            slab.handler, plan, device=local_rank, precision=args.precision,
+                            brick=tuple(args.brick), slab_z0=z0, global_cells_z=cells[2])
+    group = slabs.SlabGroup([op])
+    n_local = slab.handler.n_dofs
+    n_global = int(np.prod([c * p + 1 for c in cells]))
+    # seeded RHS of the global problem in lattice order, restricted to the slab
+    rng = np.random.default_rng(0)
+    NX, NY = cells[0] * p + 1, cells[1] * p + 1
+    plane = NX * NY
+    rng.uniform(-1.0, 1.0, z0 * p * plane)                      # skip the lower slabs' part of the stream
+    vals = rng.uniform(-1.0, 1.0, (nzg * p + 1) * plane)
+    b = vals[slab.global_nodes - z0 * p * plane]
+    b[slab.handler.constrained_dofs] = 0.0
+    b_dev = torch.from_numpy(b).cuda()
+    x_dev = torch.empty_like(b_dev)
+    cfg = SolverConfig(fixed_iterations=args.iters)
+    lib_stream = torch.cuda.ExternalStream(_lib.stream_handle(local_rank))
+
+    def step():
+        return group.solve(args.variant, [b_dev.data_ptr()], cfg, location=1, xs=[x_dev.data_ptr()])[0]
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    launches = 0
+    e0.record(lib_stream)
+    for _ in range(args.steps):
+        res = step()
+        launches += res.device_stats["kernel_launches"]
+    e1.record(lib_stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    clocks = sampler.stop()
+    if rank == 0:
+        value = n_global * args.iters * args.steps / (ms_total * 1e-3)
+        peak, peak_src = measured_peak()
+        info = op.info()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
+            "data": "synthetic (uniform[-1,1] RHS, seed 0, constrained entries zeroed)",
+            "config": workload_config(args, world),
+            "roofline": {"bound": "hbm", "kernel": "whole merged iteration, all GPUs",
+                         "achieved": value * BYTES_PER_DOF_IT / 1e9, "peak": peak * world, "unit": "GB/s",
+                         "frac": value * BYTES_PER_DOF_IT / 1e9 / (peak * world), "peak_source": peak_src,
+                         "traffic": None},
+            "cpu_baseline": None,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                    "note": "per-rank slabs stay device resident in the multi-GPU run; the host round trip is "
+                            "measured at N=1"},
+            "gpu_launches": int(launches), "clocks": clocks,
+            "extra": {"final_relative_residual": res.residual, "dofs_per_gpu": n_local,
+                      "plane_bytes_per_exchange": 8 * plane, "bricks_per_gpu": info["n_bricks"],
+                      "timer": "CUDA events on each rank's library stream, max over ranks"},
+        }
+        print(json.dumps(line))
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -233,9 +323,10 @@ def main():
     import torch
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a B200: the hot path has no CPU fallback")
-    if world > 1:
-        raise SystemExit("multi-GPU slabs: run through bench_slabs (not built in this revision)")
     torch.cuda.set_device(local_rank)
+    if world > 1:
+        run_slabs(args, rank, local_rank, world)
+        return
     from paper_2205_08909_b200 import _lib
     from paper_2205_08909_b200.mesh import GeometryVariant
     from paper_2205_08909_b200.operator import MatrixFreeOperator, OperatorSpec

@@ -477,7 +477,7 @@ static int group_sums(mfcg_op** ops, int n, int count, double* d_global) {
   Ctx* c = ops[0]->common.ctx;
   for (int i = 0; i < n; ++i) k_add_sums<<<1, 32, 0, c->stream>>>(d_global, ops[i]->engine->g_sums(), count, i == 0);
   MFCG_CUDA(cudaGetLastError());
-  if (c->nccl_comm && c->n_ranks > 1)
+  if (c->nccl_comm)  // also with one rank: keeps the collective path exercised
     MFCG_NCCL(g_nccl.AllReduce(d_global, d_global, (size_t)count, kNcclFloat64, kNcclSum, c->nccl_comm, c->stream));
   return MFCG_OK;
 }

@@ -146,3 +146,22 @@ def test_slab_group_equals_single_slab_on_one_gpu(cells, p, G, deform):
     one = S.solve("combined_pcg", op1, b, minv=op1.compute_diagonal(), config=S.SolverConfig(tolerance=1e-7))
     many = group.solve("combined_pcg", [b[gl] for gl in maps], S.SolverConfig(tolerance=1e-7))
     assert all(abs(r.iterations - one.iterations) <= 1 and r.converged for r in many)
+
+
+@pytest.mark.gpu
+def test_nccl_binding_single_rank():
+    """The run-time NCCL binding (dlopen of the libnccl torch ships): unique id, communicator with
+    one rank, and the seven-sum all-reduce inside a one-slab group solve."""
+    import torch  # noqa: F401  (loads libnccl.so.2 into the process)
+    from paper_2205_08909_b200 import solvers as S
+    uid = slabs.new_unique_id()
+    assert len(uid) == 128 and any(uid)
+    slabs.init_comm(0, uid, 0, 1)
+    m, h, plan = host_tables((5, 4, 6), 3)
+    op = gpu_operator(m, h, plan, 3, 4)
+    b = seeded_rhs(h)
+    cfg = S.SolverConfig(fixed_iterations=25)
+    one = S.solve("combined_pcg", op, b, minv=op.compute_diagonal(), config=cfg)
+    grp = slabs.SlabGroup([op]).solve("combined_pcg", [b], cfg)[0]
+    assert rel(hist_array(grp.history), hist_array(one.history)) < 1e-12
+    assert rel(grp.x, one.x) < 1e-12
