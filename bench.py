@@ -309,7 +309,7 @@ def main():
                     choices=["affine", "final_tensor_load", "inverse_jacobian_load", "quadratic_compute"])
     ap.add_argument("--deform", type=float, default=0.0)
     ap.add_argument("--ref-cells", type=int, default=32)
-    ap.add_argument("--ref-iters", type=int, default=10)
+    ap.add_argument("--ref-iters", type=int, default=60)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))

@@ -481,12 +481,17 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
         if (ptid == 4 && xmode) prefetch_l2_run(X, first, count, g.n_dofs);
       }
     };
-    constexpr int PF = 2;  // layers of L2 prefetch distance
+    // L2 prefetch distance in layers.  Measured (profiles/r01_notes.md): no gain in time and
+    // +0.9 GB of DRAM reads per launch at 73^3 (lines fetched twice), so it is off by default.
+#ifndef MFCG_L2_PREFETCH
+#define MFCG_L2_PREFETCH 0
+#endif
+    constexpr int PF = MFCG_L2_PREFETCH;
     for (int Lq = 0; Lq < PF; ++Lq) prefetch_layer(Lq);
     MFCG_TIC(tp);
     for (int L = 0; L < bcz + 2; ++L) {
       const int stage = L & 1;
-      prefetch_layer(L + PF);
+      if (PF > 0) prefetch_layer(L + PF);
       if (L >= 2) mbar_wait(&bars[2 + stage], ((L >> 1) - 1) & 1);  // layer L-2 consumed
       MFCG_TOC(tp, 0);
       if (L < bcz) {
