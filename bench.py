@@ -395,7 +395,12 @@ def main():
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
         try:
-            roofline["traffic"] = json.loads(prof.read_text()).get("k_brick_merged_bytes_per_launch")
+            # ncu capture is taken at 73^3 cells (same kernel, same brick shape); DRAM bytes per DoF
+            # are size independent above L2, so the per-launch figure is scaled to this workload
+            tj = json.loads(prof.read_text())
+            if args.geometry == "affine" and args.degree == 5 and args.precision == "fp64":
+                roofline["traffic"] = tj["bytes_per_dof"] * n
+                roofline["traffic_source"] = "profiles/traffic.json: " + tj["source"] + f"; {tj['workload']}, scaled by n_dofs"
         except Exception:
             pass
 
