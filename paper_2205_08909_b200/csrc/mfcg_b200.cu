@@ -231,7 +231,7 @@ static int op_create_impl(mfcg_ctx* ctx, const mfcg_op_desc* d, mfcg_op* op) {
     g.B[k] = std::min(b, g.cells[k]);
   }
   {
-    int bz = d->brick[2] > 0 ? d->brick[2] : std::min(8, g.cells[2]);
+    int bz = d->brick[2] > 0 ? d->brick[2] : std::min(16, g.cells[2]);
     bz = std::min(bz, g.cells[2]);
     if (d->brick[2] <= 0) {
       auto count = [&](int z) {

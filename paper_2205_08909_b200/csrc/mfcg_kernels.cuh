@@ -113,8 +113,12 @@ MFCG_CFG(8, 1, 2, 2, 32, 256, 3, 2)
 
 template <int P, int G = 0> struct Geo {
   static constexpr int N = P + 1;
-  static constexpr int RS = (N % 2 == 0) ? N + 1 : N;  // odd row stride: conflict-free 64-bit columns
-  static constexpr int TILE = N * N * RS;
+  // tile strides: element (k, j, i) of a cell tile sits at k*PSTR + j*RS + i; odd row stride.
+  // (Dense rows with planes padded to 38 doubles plus permuted line orders make the y and z
+  // sweeps bank-conflict free for N = 6, but measured 7 % slower: profiles/r01_notes.md.)
+  static constexpr int RS = (N % 2 == 0) ? N + 1 : N;
+  static constexpr int PSTR = N * RS;
+  static constexpr int TILE = N * PSTR;
   static constexpr int NTILE = G ? 3 : 2;               // scratch tiles per cell
   static constexpr int NCELL = Cfg<P, G>::BX * Cfg<P, G>::BY;
   static constexpr int WX = (P * Cfg<P, G>::BX + 1) | 1; // window row stride, odd
@@ -310,33 +314,14 @@ __device__ __forceinline__ void tensor6(const double* inv, double jxw, double* g
 
 // ---------------------------------------------------------------------------
 // Line order of the sweeps.  A math thread q of a cell handles lines order(t*TPC+q),
-// t = 0,1,...  With TPC = 16 one half-warp (the unit of a 64-bit shared-memory
-// access) works on one cell, and the order below makes the 16 lines of every pass
-// fall into 16 different banks for the tile strides RS = 7, plane = 42 doubles
-// (tools: the search is reproduced in DESIGN.md section 5).  -1 = idle lane.
+// t = 0,1,...; -1 = idle lane.  The order decides which shared-memory banks the 16 lanes of a
+// half-warp (the unit of a 64-bit access) hit.
 template <int N> struct LineOrder {
   static constexpr bool custom = false;
   __device__ static __forceinline__ int x(int s, int tpc) { return s < N * N ? s : -1; }
   __device__ static __forceinline__ int y(int s, int tpc) { return s < N * N ? s : -1; }
   __device__ static __forceinline__ int z(int s, int tpc) { return s < N * N ? s : -1; }
 };
-template <> struct LineOrder<6> {
-  static constexpr bool custom = true;
-  __device__ static __forceinline__ int x(int s, int tpc) { return s < 36 ? s : -1; }
-  __device__ static __forceinline__ int y(int s, int tpc) {
-    if (tpc != 16) return s < 36 ? s : -1;
-    constexpr signed char t[48] = {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 14, 15, 16, 17, 12, 13, 18, 19, 20, 21, 22, 23,
-                                   24, 25, 26, 27, 28, 29, 34, 35, 30, 31, 32, 33, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
-    return t[s];
-  }
-  __device__ static __forceinline__ int z(int s, int tpc) {
-    if (tpc != 16) return s < 36 ? s : -1;
-    constexpr signed char t[48] = {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 19, 25, 14, 15, 16, 17, 18, 20, 21, 22,
-                                   23, 24, 26, 27, 31, 33, -1, -1, 28, 29, 30, 32, 34, 35, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
-    return t[s];
-  }
-};
-
 // ---------------------------------------------------------------------------
 // mbarrier / named-barrier helpers (shared::cta)
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -402,7 +387,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
         const T* __restrict__ src, T* __restrict__ Pv,
         T* __restrict__ V, T* __restrict__ R, T* __restrict__ X, const T* __restrict__ Minv,
         const SolveState* __restrict__ st, double* __restrict__ partials, int brick_offset) {
-  constexpr int N = P + 1, RS = Geo<P, G>::RS, TILE = Geo<P, G>::TILE, WX = Geo<P, G>::WX,
+  constexpr int N = P + 1, RS = Geo<P, G>::RS, PSTR = Geo<P, G>::PSTR, TILE = Geo<P, G>::TILE, WX = Geo<P, G>::WX,
                 PLANE = Geo<P, G>::PLANE, NCELL = Geo<P, G>::NCELL, RB = Geo<P, G>::RB,
                 NT_C = Cfg<P, G>::NT_C, NT_P = Cfg<P, G>::NT_P, KC = Cfg<P, G>::KC, HE = EOShape<N>::HE;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -657,9 +642,9 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
         //   x lines (k,j): l*RS, 1;  y lines (k,i): k*N*RS + i, RS;  z lines (j,i): j*RS + i, N*RS
         auto line_base = [&](int dir, int l) {
           const int hi = l / N, lo = l - hi * N;
-          return dir == 0 ? l * RS : (dir == 1 ? hi * N * RS + lo : hi * RS + lo);
+          return dir == 0 ? hi * PSTR + lo * RS : (dir == 1 ? hi * PSTR + lo : hi * RS + lo);
         };
-        constexpr int STR[3] = {1, RS, N * RS};
+        constexpr int STR[3] = {1, RS, PSTR};
         // out-of-place or in-place 1D operator on the owned lines of direction dir
         auto sweep = [&](int dir, int kind, bool tr, bool acc, const T* srct, int sstride_unused, T* dstt) {
           (void)sstride_unused;
@@ -701,7 +686,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             eo_apply_sym<N>(gen.Se, gen.So, false, e, o, se, so);
             eo_join<N>(se, so, out);
 #pragma unroll
-            for (int i = 0; i < N; ++i) At[l * RS + i] = out[i];
+            for (int i = 0; i < N; ++i) At[k * PSTR + j * RS + i] = out[i];
           }
         }
         math_barrier<NT_C>();
@@ -725,7 +710,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             const int base = j * RS + i;
             T u[N], e[HE], o[HE], se[HE], so[HE], gz[N], fz[N];
 #pragma unroll
-            for (int k = 0; k < N; ++k) u[k] = At[base + k * N * RS];
+            for (int k = 0; k < N; ++k) u[k] = At[base + k * PSTR];
             eo_split<N>(u, e, o);
             eo_apply_anti<N>(gen.Be, gen.Bo, false, e, o, se, so);
             eo_join<N>(se, so, gz);
@@ -761,16 +746,16 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
 #pragma unroll
                 for (int c = 0; c < 6; ++c) G6[c] = (T)g6d[c];
               }
-              const T gx = Bt[base + k * N * RS], gy = Ct[base + k * N * RS], gzz = gz[k];
-              Bt[base + k * N * RS] = G6[0] * gx + G6[3] * gy + G6[4] * gzz;
-              Ct[base + k * N * RS] = G6[3] * gx + G6[1] * gy + G6[5] * gzz;
+              const T gx = Bt[base + k * PSTR], gy = Ct[base + k * PSTR], gzz = gz[k];
+              Bt[base + k * PSTR] = G6[0] * gx + G6[3] * gy + G6[4] * gzz;
+              Ct[base + k * PSTR] = G6[3] * gx + G6[1] * gy + G6[5] * gzz;
               fz[k] = G6[4] * gx + G6[5] * gy + G6[2] * gzz;
             }
             eo_split<N>(fz, e, o);
             eo_apply_anti<N>(gen.Be, gen.Bo, true, e, o, se, so);
             eo_join<N>(se, so, u);
 #pragma unroll
-            for (int k = 0; k < N; ++k) At[base + k * N * RS] = u[k];
+            for (int k = 0; k < N; ++k) At[base + k * PSTR] = u[k];
           }
         }
         math_barrier<NT_C>();
@@ -800,8 +785,8 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
   #pragma unroll
             for (int i = 0; i < N; ++i) u[i] = row[i];
             eo_split<N>(u, e, o);
-            T* ao = At + l * RS;
-            T* bo = Bt + l * RS;
+            T* ao = At + k * PSTR + j * RS;
+            T* bo = Bt + k * PSTR + j * RS;
             T se[HE], so[HE], out[N];
   #pragma unroll
             for (int i = 0; i < HE; ++i) { se[i] = 0; so[i] = 0; }
@@ -830,8 +815,8 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             const int l = LineOrder<N>::y(q + t * TPC, TPC);
             if (l < 0) continue;
             const int k = l / N, i = l - k * N;
-            T* ac = At + k * N * RS + i;
-            T* bc = Bt + k * N * RS + i;
+            T* ac = At + k * PSTR + i;
+            T* bc = Bt + k * PSTR + i;
             T a[N], ea[HE], oa[HE], eb[HE], ob[HE];
   #pragma unroll
             for (int j = 0; j < N; ++j) a[j] = ac[j * RS];
@@ -872,10 +857,10 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             const T* bc = Bt + j * RS + i;
             T a[N], ec[HE], oc[HE], ed[HE], od[HE];
   #pragma unroll
-            for (int k = 0; k < N; ++k) a[k] = ac[k * N * RS];
+            for (int k = 0; k < N; ++k) a[k] = ac[k * PSTR];
             eo_split<N>(a, ec, oc);
   #pragma unroll
-            for (int k = 0; k < N; ++k) a[k] = bc[k * N * RS];
+            for (int k = 0; k < N; ++k) a[k] = bc[k * PSTR];
             eo_split<N>(a, ed, od);
             T se[HE], so[HE], out[N];
   #pragma unroll
@@ -886,7 +871,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             eo_mul<N>(tab.Me, tab.Mo, ed, od, se, so);  // + M de
             eo_join<N>(se, so, out);
   #pragma unroll
-            for (int k = 0; k < N; ++k) ac[k * N * RS] = out[k];
+            for (int k = 0; k < N; ++k) ac[k * PSTR] = out[k];
           }
         }
         MFCG_TOC(tc, 7);
@@ -920,10 +905,10 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
 #pragma unroll
         for (int k = 0; k <= P; ++k) {
           T sum = 0;
-          if (o00 >= 0) sum += A[o00 + k * N * RS];
-          if (o01 >= 0) sum += A[o01 + k * N * RS];
-          if (o10 >= 0) sum += A[o10 + k * N * RS];
-          if (o11 >= 0) sum += A[o11 + k * N * RS];
+          if (o00 >= 0) sum += A[o00 + k * PSTR];
+          if (o01 >= 0) sum += A[o01 + k * PSTR];
+          if (o10 >= 0) sum += A[o10 + k * PSTR];
+          if (o11 >= 0) sum += A[o11 + k * PSTR];
           if (k == 0) sum += carry[j * WX + i];
           if (k == P && L < bcz - 1) {
             carry[j * WX + i] = sum;
