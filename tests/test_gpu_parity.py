@@ -267,3 +267,36 @@ def test_curved_midsize_vs_oracle_and_errors():
     a = gpu_operator(m0, h0, plan0, 3, 4).apply(u0)
     f = gpu_operator(m0, h0, plan0, 3, 4, variant="final_tensor_load").apply(u0)
     assert rel(f, a) < 1e-12
+
+
+# ---------------------------------------------------------------------------
+# BASELINE sizes: no oracle can run there, so size-independent properties (the prompt's
+# "encode -> decode round trips, linearity, checksums"): true vs recurred residual, merged vs
+# standard scalars, linearity of the operator, constrained rows copied through bit-exactly.
+
+
+@pytest.mark.parametrize("n", [73, 116])
+def test_full_size_properties(n):
+    """Q5 at 73^3 (4.9e7 DoFs, the >= 5e7 target size) and 116^3 (1.96e8 DoFs, top rung of configs[1])."""
+    S = _solvers()
+    p = 5
+    m, h, plan = host_tables((n, n, n), p)
+    op = gpu_operator(m, h, plan, p, p + 1)
+    b = seeded_rhs(h)
+    minv = op.compute_diagonal()
+    iters = 30
+    mer = S.solve("combined_pcg", op, b, minv=minv, config=S.SolverConfig(fixed_iterations=iters))
+    std = S.solve("pcg", op, b, minv=minv, config=S.SolverConfig(fixed_iterations=iters))
+    Hm, Hs = hist_array(mer.history), hist_array(std.history)
+    assert rel(Hm[:, 0], Hs[:, 0]) < 1e-8 and rel(Hm[:, 1], Hs[:, 1]) < 1e-8   # alpha, beta
+    assert rel(Hm[:, 3], Hs[:, 3]) < 1e-8                                       # residual history
+    bn = np.linalg.norm(b)
+    Ax = op.apply(mer.x)
+    assert abs(np.linalg.norm(b - Ax) / bn - mer.residual) < 1e-9               # recurred == true residual
+    assert np.array_equal(Ax[h.constrained_dofs], mer.x[h.constrained_dofs])    # identity rows, bit-exact
+    assert rel(mer.x, std.x) < 1e-7
+    # linearity: A(2x - 3b) == 2 Ax - 3 Ab
+    Ab = op.apply(b)
+    assert rel(op.apply(2.0 * mer.x - 3.0 * b), 2.0 * Ax - 3.0 * Ab) < 1e-12
+    # energy checksum: x.b == x.A x up to the residual (symmetric positive operator)
+    assert abs(mer.x @ Ax - mer.x @ b) <= 2 * mer.residual * bn * np.linalg.norm(mer.x)
