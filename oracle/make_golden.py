@@ -193,8 +193,16 @@ def curved():
     np.savez_compressed(OUT / "curved.npz", **out)
 
 
+def harness_rhs():
+    """Manufactured right-hand side of BP5, p = 3, (3,2,2) cells, deformation 0.05."""
+    from mfcg.bench import assemble_problem
+    _, b, _ = assemble_problem("BP5", 3, (3, 2, 2))
+    np.savez_compressed(OUT / "harness.npz", bp5_p3_322_rhs=b)
+
+
 if __name__ == "__main__":
     tables()
+    harness_rhs()
     numbering()
     apply_cases()
     config1()
