@@ -150,6 +150,8 @@ class Engine : public EngineBase {
       smem_ = (int)Geo<P, 1>::template smem_bytes<T>();
       MFCG_CUDA(cudaFuncSetAttribute(k_brick<P, T, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
       MFCG_CUDA(cudaFuncSetAttribute(k_brick<P, T, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
+      MFCG_CUDA(cudaFuncSetAttribute(k_brick<P, T, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
+      MFCG_CUDA(cudaFuncSetAttribute(k_brick<P, T, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
       int rc = build_general_tables();
       if (rc) return rc;
     } else {
@@ -340,12 +342,19 @@ class Engine : public EngineBase {
       else
         k_brick<P, T, 1, 0><<<nb, Cfg<P, 0>::THREADS, smem_, stream()>>>(
             c_->grid, tab_, gen_, geo_, nullptr, pv, v, r_, x_, minv_, c_->d_state, partials, off);
-    } else {
+    } else if (c_->geometry != MFCG_GEOM_QUADRATIC_COMPUTE) {
       if (mode == 0)
         k_brick<P, T, 0, 1><<<nb, Cfg<P, 1>::THREADS, smem_, stream()>>>(
             c_->grid, tab_, gen_, geo_, src, nullptr, v, nullptr, nullptr, nullptr, nullptr, nullptr, off);
       else
         k_brick<P, T, 1, 1><<<nb, Cfg<P, 1>::THREADS, smem_, stream()>>>(
+            c_->grid, tab_, gen_, geo_, nullptr, pv, v, r_, x_, minv_, c_->d_state, partials, off);
+    } else {
+      if (mode == 0)
+        k_brick<P, T, 0, 2><<<nb, Cfg<P, 2>::THREADS, smem_, stream()>>>(
+            c_->grid, tab_, gen_, geo_, src, nullptr, v, nullptr, nullptr, nullptr, nullptr, nullptr, off);
+      else
+        k_brick<P, T, 1, 2><<<nb, Cfg<P, 2>::THREADS, smem_, stream()>>>(
             c_->grid, tab_, gen_, geo_, nullptr, pv, v, r_, x_, minv_, c_->d_state, partials, off);
     }
     MFCG_CUDA(cudaGetLastError());

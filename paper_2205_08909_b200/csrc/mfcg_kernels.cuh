@@ -111,6 +111,17 @@ MFCG_CFG(6, 1, 3, 2, 25, 224, 3, 2)
 MFCG_CFG(7, 1, 2, 2, 32, 256, 3, 2)
 MFCG_CFG(8, 1, 2, 2, 32, 256, 3, 2)
 
+// G = 2: the 27-node on-the-fly variant (same shapes; separate instantiation keeps its registers
+// out of the stored-geometry kernels)
+MFCG_CFG(1, 2, 16, 16, 1, 96, 3, 2)
+MFCG_CFG(2, 2, 10, 10, 3, 96, 3, 2)
+MFCG_CFG(3, 2, 6, 6, 8, 96, 3, 2)
+MFCG_CFG(4, 2, 5, 5, 9, 96, 3, 2)
+MFCG_CFG(5, 2, 4, 3, 12, 96, 3, 2)
+MFCG_CFG(6, 2, 3, 2, 25, 96, 3, 2)
+MFCG_CFG(7, 2, 2, 2, 32, 128, 3, 2)
+MFCG_CFG(8, 2, 2, 2, 32, 128, 3, 2)
+
 template <int P, int G = 0> struct Geo {
   static constexpr int N = P + 1;
   // tile strides: element (k, j, i) of a cell tile sits at k*PSTR + j*RS + i; odd row stride.
@@ -635,7 +646,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
       mbar_wait(&bars[stage], (L >> 1) & 1);  // layer L full
       MFCG_TOC(tc, 4);
 
-      if (G == 1) {
+      if (G >= 1) {
         // ===== general coefficient tensor: 12 sweeps + pointwise flux (operator.py:253-281) =====
         T* const Ct = Bs + NCELL * TILE + cell * TILE;  // third tile of the cell
         // line l of a sweep direction: base offset and element stride inside a tile
@@ -718,13 +729,13 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             for (int k = 0; k < N; ++k) {
               const int qp = (k * N + j) * N + i;
               T G6[6];
-              if (geo.kind == 1) {
+              if (G == 1 && geo.kind == 1) {
                 const T* gp = reinterpret_cast<const T*>(geo.data) + ((i64)cellg * NQ3 + qp) * 6;
 #pragma unroll
                 for (int c = 0; c < 6; ++c) G6[c] = gp[c];
               } else {
                 double inv[9], jxw, g6d[6];
-                if (geo.kind == 2) {
+                if (G == 1) {
                   const T* ip = reinterpret_cast<const T*>(geo.data) + ((i64)cellg * NQ3 + qp) * 9;
 #pragma unroll
                   for (int c = 0; c < 9; ++c) inv[c] = (double)ip[c];
