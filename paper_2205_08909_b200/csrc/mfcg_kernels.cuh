@@ -24,6 +24,15 @@
 #define MFCG_SKIP 0  // debug only: 1 skip sweeps, 2 skip gather, 4 skip post, 8 skip fill loads
 #endif
 
+// Debug build (-DMFCG_BOUNDS): index checks on every global / shared access of the brick kernel;
+// a violation traps, which the host sees as a CUDA error.  (compute-sanitizer is closed on the
+// GPU pool this was developed on.)
+#ifdef MFCG_BOUNDS
+#define MFCG_CHECK(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define MFCG_CHECK(cond)
+#endif
+
 namespace mfcg {
 
 typedef long long i64;
@@ -506,6 +515,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             rr[c] = vv[c] = pp[c] = mm[c] = xx[c] = (T)0;
             if (it < nitem) {
               const i64 gi = gbase + it;
+              MFCG_CHECK(gi >= 0 && gi < n_int);
               if (MODE == 0) {
                 pp[c] = src[gi];
               } else {
@@ -538,6 +548,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             const int rem2 = it - kk * nint2d;
             const int jm = (int)(((unsigned)rem2 * lxm_magic) >> 16);
             const int im = rem2 - jm * lxm;
+            MFCG_CHECK(kk >= 0 && Kfirst + kk <= Klast && jm >= 0 && jm < Ly - 1 && im >= 0 && im < Lx - 1);
             ring[((Kfirst + kk) % RB) * PLANE + (jm + 1) * WX + im + 1] = val;
           }
         }
@@ -566,6 +577,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
                 const int K = L * P + k0 + kk;
                 const int ez = K == 0 ? 0 : (K == Lz ? 2 : 1);
                 const i64 gi = st27[ex + 3 * ey + 9 * ez] + ox + lx * oy + (ez == 1 ? (i64)(lx * ly) * (K - 1) : 0);
+                MFCG_CHECK(gi >= n_int && gi < g.n_dofs && i >= 0 && i <= Lx && j >= 0 && j <= Ly && K >= 0 && K <= Lz);
                 pp[c] = MODE == 0 ? src[gi] : Pv[gi];
                 mk[c] = g.mask[gi - n_int] & 1;
                 dst[c] = (K % RB) * PLANE + j * WX + i;
@@ -583,6 +595,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
           const i64 fb = st27[side == 0 ? 4 : 22];
           const int slot = ((side == 0 ? 0 : Lz) % RB) * PLANE;
           for (int it = ptid; it < nint2d; it += NT_P) {
+            MFCG_CHECK(fb + it >= n_int && fb + it < g.n_dofs);
             const T pv = MODE == 0 ? src[fb + it] : Pv[fb + it];
             const unsigned char mk = g.mask[fb + it - n_int] & 1;
             const int jm = (int)(((unsigned)it * lxm_magic) >> 16);
@@ -609,6 +622,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             rr[c] = vv[c] = pp[c] = mm[c] = (T)0;
             if (it < nitem) {
               const i64 gi = gbase + it;
+              MFCG_CHECK(gi >= 0 && gi < n_int);
               rr[c] = R[gi]; vv[c] = V[gi]; pp[c] = Pv[gi]; mm[c] = Minv[gi];
             }
           }
@@ -929,6 +943,8 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
           const int ez = K == 0 ? 0 : (K == Lz ? 2 : 1);
           const i64 gi = st27[e2 + 9 * ez] + o2 + (ez == 1 ? (i64)pstride * (K - 1) : 0);
           // constrained rows receive garbage here; k_post / k_surface_fix restore v_c = p_c
+          MFCG_CHECK((edge || ez != 1) ? (gi >= n_int && gi < g.n_dofs) : (gi >= 0 && gi < n_int));
+          MFCG_CHECK(o11 < NCELL * TILE && o10 < NCELL * TILE && o01 < NCELL * TILE && o00 < NCELL * TILE);
           if (!(edge || ez != 1)) V[gi] = sum;
           else atomicAdd(&V[gi], sum);
         }
