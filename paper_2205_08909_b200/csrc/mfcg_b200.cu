@@ -38,10 +38,6 @@ EngineBase* make_engine(OpCommon* c, int* status) {
   return nullptr;
 }
 
-// default brick extent in x / y per geometry class and degree == Cfg<P, G>::BX / BY (mfcg_kernels.cuh)
-static const int kBrickX[2][9] = {{0, 16, 10, 6, 5, 4, 3, 2, 2}, {0, 16, 10, 6, 5, 4, 3, 2, 2}};
-static const int kBrickY[2][9] = {{0, 16, 10, 6, 5, 4, 3, 2, 2}, {0, 16, 10, 6, 5, 3, 2, 2, 2}};
-
 }  // namespace mfcg
 
 // ---------------------------------------------------------------------------
@@ -225,7 +221,9 @@ static int op_create_impl(mfcg_ctx* ctx, const mfcg_op_desc* d, mfcg_op* op) {
   // brick extents: x, y bounded by the kernel's shared-memory window; z free
   for (int k = 0; k < 2; ++k) {
     const int gclass = d->geometry == MFCG_GEOM_AFFINE ? 0 : 1;
-    const int cap = k == 0 ? kBrickX[gclass][p] : kBrickY[gclass][p];
+    int capx = 1, capy = 1;
+    brick_caps(p, gclass, &capx, &capy);
+    const int cap = k == 0 ? capx : capy;
     int b = d->brick[k] > 0 ? d->brick[k] : cap;
     if (b > cap) { set_error("brick extent in x/y exceeds the kernel window for this degree"); return MFCG_EINVAL; }
     g.B[k] = std::min(b, g.cells[k]);

@@ -86,11 +86,15 @@ struct SolveState {
 // "memory" threads (all global loads: pre on the way in, post one layer behind),
 // KC points per load batch of a memory thread (memory-level parallelism).
 template <int P, int G = 0> struct Cfg;
-#define MFCG_CFG(P_, G_, BX_, BY_, TPC_, TP_, KC_, MB_)                                        \
+#define MFCG_CFG_X(P_, G_, BX_, BY_, TPC_, TP_, KC_, MB_, OC_)                                 \
   template <> struct Cfg<P_, G_> {                                                             \
     static constexpr int BX = BX_, BY = BY_, TPC = TPC_, NT_P = TP_, KC = KC_, MINB = MB_,     \
                          NT_C = ((BX_ * BY_ * TPC_ + 31) / 32) * 32, THREADS = NT_C + TP_;     \
+    /* ONCHIP: r' and 1/diag of the layers in flight stay in shared-memory rings and the seven   \
+       post sums are taken by the math warps in the gather (no re-read through L2) */            \
+    static constexpr bool ONCHIP = OC_;                                                        \
   };
+#define MFCG_CFG(P_, G_, BX_, BY_, TPC_, TP_, KC_, MB_) MFCG_CFG_X(P_, G_, BX_, BY_, TPC_, TP_, KC_, MB_, false)
 // TPC = math threads per cell; each owns ceil((P+1)^2 / TPC) lines of that cell in every sweep.
 // G = 0: separable cell operator on affine meshes (two tiles per cell);
 // G = 1: general coefficient tensor per quadrature point (three tiles per cell, smaller bricks).
@@ -107,7 +111,18 @@ MFCG_CFG(4, 0, 5, 5, 9, 288, 3, 2)
 #ifndef MFCG_NTP5
 #define MFCG_NTP5 320
 #endif
+#ifndef MFCG_V7
+#define MFCG_V7 0
+#endif
+#if MFCG_V7
+#ifndef MFCG_V7_BX
+#define MFCG_V7_BX 3
+#define MFCG_V7_BY 3
+#endif
+MFCG_CFG_X(5, 0, MFCG_V7_BX, MFCG_V7_BY, MFCG_TPC5, MFCG_NTP5, MFCG_KC5, 2, true)
+#else
 MFCG_CFG(5, 0, 4, 4, MFCG_TPC5, MFCG_NTP5, MFCG_KC5, 2)
+#endif
 MFCG_CFG(6, 0, 3, 3, 25, 256, 3, 2)
 MFCG_CFG(7, 0, 2, 2, 32, 256, 3, 2)
 MFCG_CFG(8, 0, 2, 2, 32, 256, 3, 2)
@@ -131,6 +146,20 @@ MFCG_CFG(6, 2, 3, 2, 25, 96, 3, 2)
 MFCG_CFG(7, 2, 2, 2, 32, 128, 3, 2)
 MFCG_CFG(8, 2, 2, 2, 32, 128, 3, 2)
 
+// largest brick extents in x / y the kernel's shared-memory window allows (host side)
+inline bool brick_caps(int p, int gclass, int* bx, int* by) {
+  switch (p) {
+#define MFCG_CAP(P_)                                                   \
+  case P_:                                                             \
+    *bx = gclass ? Cfg<P_, 1>::BX : Cfg<P_, 0>::BX;                    \
+    *by = gclass ? Cfg<P_, 1>::BY : Cfg<P_, 0>::BY;                    \
+    return true;
+    MFCG_CAP(1) MFCG_CAP(2) MFCG_CAP(3) MFCG_CAP(4) MFCG_CAP(5) MFCG_CAP(6) MFCG_CAP(7) MFCG_CAP(8)
+#undef MFCG_CAP
+  }
+  return false;
+}
+
 template <int P, int G = 0> struct Geo {
   static constexpr int N = P + 1;
   // tile strides: element (k, j, i) of a cell tile sits at k*PSTR + j*RS + i; odd row stride.
@@ -144,8 +173,9 @@ template <int P, int G = 0> struct Geo {
   static constexpr int WX = (P * Cfg<P, G>::BX + 1) | 1; // window row stride, odd
   static constexpr int PLANE = WX * (P * Cfg<P, G>::BY + 1);
   static constexpr int RB = 2 * P + 1;                  // lattice planes in the ring: two layers share one
+  static constexpr int NRING = Cfg<P, G>::ONCHIP ? 3 : 1;  // p' (+ r', 1/diag)
   template <typename T> __host__ __device__ static constexpr size_t red_offset() {
-    return (256 + sizeof(T) * (size_t)(RB * PLANE + PLANE + NTILE * NCELL * TILE) + 15) & ~(size_t)15;
+    return (256 + sizeof(T) * (size_t)(NRING * RB * PLANE + PLANE + NTILE * NCELL * TILE) + 15) & ~(size_t)15;
   }
   template <typename T> __host__ __device__ static constexpr size_t smem_bytes() { return red_offset<T>() + 8 * 7 * 32; }
 };
@@ -413,8 +443,11 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
   extern __shared__ __align__(16) unsigned char smem_raw[];
   i64* st27 = reinterpret_cast<i64*>(smem_raw);                               // 27 entity starts
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem_raw + 224);  // full[2], empty[2]
+  constexpr bool ONCHIP = Cfg<P, G>::ONCHIP && MODE == 1;
   T* ring = reinterpret_cast<T*>(smem_raw + 256);
-  T* carry = ring + RB * PLANE;
+  T* Rring = ring + RB * PLANE;              // only with Cfg::ONCHIP
+  T* Mring = Rring + RB * PLANE;
+  T* carry = ring + Geo<P, G>::NRING * RB * PLANE;
   T* A = carry + PLANE;
   T* Bs = A + NCELL * TILE;
   constexpr size_t RED_OFF = Geo<P, G>::template red_offset<T>();
@@ -466,7 +499,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
     const unsigned n2d_magic = nint2d > 0 ? (unsigned)((0x100000000ull + nint2d - 1) / nint2d) : 0u;
     const unsigned per_magic = (unsigned)((0x100000000ull + nperim - 1) / nperim);
     const i64 st_int = st27[13];
-    if ((ptid & 31) == 0)
+    if (!ONCHIP && (ptid & 31) == 0)
       for (int q = 0; q < 7; ++q) red[pwarp * 7 + q] = 0.0;
     // interior run of layer Lq in every vector: [run_first(Lq), +run_count(Lq))
     auto prefetch_layer = [&](int Lq) {
@@ -529,6 +562,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             const int it = it0 + c * NT_P;
             if (it >= nitem) continue;
             T val = pp[c];
+            T rnew = (T)0;
             if (MODE == 1) {
               const i64 gi = gbase + it;
               T r = rr[c], p = pp[c];
@@ -543,13 +577,16 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
               R[gi] = r;
               Pv[gi] = p;
               val = p;
+              rnew = r;
             }
             const int kk = (int)__umulhi((unsigned)it, n2d_magic);
             const int rem2 = it - kk * nint2d;
             const int jm = (int)(((unsigned)rem2 * lxm_magic) >> 16);
             const int im = rem2 - jm * lxm;
             MFCG_CHECK(kk >= 0 && Kfirst + kk <= Klast && jm >= 0 && jm < Ly - 1 && im >= 0 && im < Lx - 1);
-            ring[((Kfirst + kk) % RB) * PLANE + (jm + 1) * WX + im + 1] = val;
+            const int rdst = ((Kfirst + kk) % RB) * PLANE + (jm + 1) * WX + im + 1;
+            ring[rdst] = val;
+            if (ONCHIP) { Rring[rdst] = rnew; Mring[rdst] = mm[c]; }
           }
         }
         // (b) brick-boundary points of the layer's planes: already pre-updated by k_pre; p only
@@ -606,7 +643,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
         mbar_arrive(&bars[stage]);  // layer L full
         MFCG_TOC(tp, 1);
       }
-      if (MODE == 1 && L >= 2 && !(MFCG_SKIP & 4)) {
+      if (MODE == 1 && !ONCHIP && L >= 2 && !(MFCG_SKIP & 4)) {
         // ---- post sums of layer L-2 (solvers.py:692-698): its v is final and, like r, p and
         // 1/diag, still resident in L2; one contiguous run per vector
         const int Lp = L - 2;
@@ -652,6 +689,8 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
     T* const At = A + cell * TILE;
     T* const Bt = Bs + cell * TILE;
     const T* const ring_cell = ring + cy * P * WX + cx * P;
+    if (ONCHIP && (tid & 31) == 0)
+      for (int qq = 0; qq < 7; ++qq) red[(tid >> 5) * 7 + qq] = 0.0;
     MFCG_TIC(tc);
     for (int L = 0; L < bcz; ++L) {
       const int stage = L & 1;
@@ -906,6 +945,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
       }
 
       // ---- gather the cells' contributions per lattice point, finish the planes
+      double s[7] = {0, 0, 0, 0, 0, 0, 0};
       for (int rem = tid; rem < ((MFCG_SKIP & 2) ? 0 : fp); rem += NT_C) {
         const int j = (int)(((unsigned)rem * fw_magic) >> 16);
         const int i = rem - j * fw;
@@ -945,9 +985,27 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
           // constrained rows receive garbage here; k_post / k_surface_fix restore v_c = p_c
           MFCG_CHECK((edge || ez != 1) ? (gi >= n_int && gi < g.n_dofs) : (gi >= 0 && gi < n_int));
           MFCG_CHECK(o11 < NCELL * TILE && o10 < NCELL * TILE && o01 < NCELL * TILE && o00 < NCELL * TILE);
-          if (!(edge || ez != 1)) V[gi] = sum;
-          else atomicAdd(&V[gi], sum);
+          if (!(edge || ez != 1)) {
+            V[gi] = sum;
+            if (ONCHIP) {  // post on values that never left the SM (solvers.py:692-698)
+              int slot = s0 + k;
+              if (slot >= RB) slot -= RB;
+              const int ro = slot * PLANE + j * WX + i;
+              const double r = (double)Rring[ro], m = (double)Mring[ro], p = (double)ring[ro], v = (double)sum;
+              const double mr = m * r, mv = m * v;
+              s[0] += r * r; s[1] += p * v; s[2] += r * v; s[3] += v * v;
+              s[4] += r * mr; s[5] += r * mv; s[6] += v * mv;
+            }
+          } else {
+            atomicAdd(&V[gi], sum);
+          }
         }
+      }
+      if (ONCHIP) {
+        warp_reduce7(s);
+        if ((tid & 31) == 0)
+#pragma unroll
+          for (int qq = 0; qq < 7; ++qq) red[(tid >> 5) * 7 + qq] += s[qq];
       }
       mbar_arrive(&bars[2 + stage]);  // layer L consumed (orders the v stores before the post loads)
       MFCG_TOC(tc, 9);
@@ -962,7 +1020,11 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
     __syncthreads();
     if (tid < 7) {
       double acc = 0.0;
-      for (int w = 0; w < NT_P / 32; ++w) acc += red[w * 7 + tid];
+      if (ONCHIP) {
+        for (int w = 0; w < NT_C / 32; ++w) acc += red[w * 7 + tid];
+      } else {
+        for (int w = 0; w < NT_P / 32; ++w) acc += red[w * 7 + tid];
+      }
       partials[(i64)b * 8 + tid] = acc;
     }
   }

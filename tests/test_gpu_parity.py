@@ -38,7 +38,7 @@ def test_apply_diag_perm_vs_fixture(golden, ci):
         op.apply(u[:-1])
 
 
-@pytest.mark.parametrize("brick", [(1, 1, 1), (2, 3, 2), (4, 4, 1), (3, 2, 5)])
+@pytest.mark.parametrize("brick", [(1, 1, 1), (2, 3, 2), (3, 3, 1), (3, 2, 5)])
 def test_apply_independent_of_brick_shape(brick):
     cells, p, nq = (7, 5, 6), 5, 6
     m, h, plan = host_tables(cells, p)
