@@ -119,7 +119,10 @@ MFCG_CFG(4, 0, 5, 5, 9, 288, 3, 2)
 #define MFCG_V7_BX 3
 #define MFCG_V7_BY 3
 #endif
-MFCG_CFG_X(5, 0, MFCG_V7_BX, MFCG_V7_BY, MFCG_TPC5, MFCG_NTP5, MFCG_KC5, 2, true)
+#ifndef MFCG_V7_MINB
+#define MFCG_V7_MINB 2
+#endif
+MFCG_CFG_X(5, 0, MFCG_V7_BX, MFCG_V7_BY, MFCG_TPC5, MFCG_NTP5, MFCG_KC5, MFCG_V7_MINB, true)
 #else
 MFCG_CFG(5, 0, 4, 4, MFCG_TPC5, MFCG_NTP5, MFCG_KC5, 2)
 #endif
@@ -372,6 +375,28 @@ template <int N> struct LineOrder {
   __device__ static __forceinline__ int y(int s, int tpc) { return s < N * N ? s : -1; }
   __device__ static __forceinline__ int z(int s, int tpc) { return s < N * N ? s : -1; }
 };
+#ifdef MFCG_LINE_ORDER
+// Experiment: line orders found by exhaustive search for the padded-row layout (RS = 7, plane 42,
+// tile 252 = 12 mod 16) and 12 threads per cell: every half-warp (12 + 4, 8 + 8, 4 + 12 lanes of
+// two cells) hits 16 different banks in the x stores and the y sweep; z stays 2-way.
+template <> struct LineOrder<6> {
+  static constexpr bool custom = true;
+  __device__ static __forceinline__ int x(int s, int tpc) {
+    if (tpc != 12) return s < 36 ? s : -1;
+    constexpr signed char t[36] = {24, 35, 26, 33, 20, 31, 22, 29, 32, 27, 34, 25, 4, 11, 6, 9, 16, 23,
+                                   18, 21, 28, 19, 30, 17, 0, 7, 2, 5, 12, 3, 14, 1, 8, 15, 10, 13};
+    return t[s];
+  }
+  __device__ static __forceinline__ int y(int s, int tpc) {
+    if (tpc != 12) return s < 36 ? s : -1;
+    constexpr signed char t[36] = {32, 33, 26, 27, 24, 25, 18, 19, 28, 29, 30, 31, 8, 9, 10, 11, 20, 21,
+                                   22, 23, 12, 13, 34, 35, 0, 1, 2, 3, 4, 5, 14, 15, 16, 17, 6, 7};
+    return t[s];
+  }
+  __device__ static __forceinline__ int z(int s, int tpc) { return s < 36 ? s : -1; }
+};
+#endif
+
 // ---------------------------------------------------------------------------
 // mbarrier / named-barrier helpers (shared::cta)
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
