@@ -803,6 +803,32 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             eo_split<N>(u, e, o);
             eo_apply_anti<N>(gen.Be, gen.Bo, false, e, o, se, so);
             eo_join<N>(se, so, gz);
+            // on-the-fly geometry: contract the cell's 27 nodes with the x / y basis of this column
+            // once (mesh.py:155-174 evaluates the same tri-quadratic map); 27 sums per column
+            double colx[9], coly[9], colv[9];
+            if (G == 2) {
+              const double* nd = reinterpret_cast<const double*>(geo.data) + (i64)cellg * 81;
+#pragma unroll
+              for (int t9 = 0; t9 < 9; ++t9) { colx[t9] = 0.0; coly[t9] = 0.0; colv[t9] = 0.0; }
+#pragma unroll
+              for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int b3 = 0; b3 < 3; ++b3) {
+                  const double vy = (double)gen.qv[j * 3 + b3], dy = (double)gen.qd[j * 3 + b3];
+#pragma unroll
+                  for (int a3 = 0; a3 < 3; ++a3) {
+                    const double vx = (double)gen.qv[i * 3 + a3], dx = (double)gen.qd[i * 3 + a3];
+                    const double wx = dx * vy, wy = vx * dy, wv = vx * vy;
+                    const double* n3 = nd + 3 * ((c * 3 + b3) * 3 + a3);
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) {
+                      colx[c * 3 + d] += n3[d] * wx;
+                      coly[c * 3 + d] += n3[d] * wy;
+                      colv[c * 3 + d] += n3[d] * wv;
+                    }
+                  }
+                }
+            }
 #pragma unroll
             for (int k = 0; k < N; ++k) {
               const int qp = (k * N + j) * N + i;
@@ -819,15 +845,20 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
                   for (int c = 0; c < 9; ++c) inv[c] = (double)ip[c];
                   jxw = (double)reinterpret_cast<const T*>(geo.jxw)[(i64)cellg * NQ3 + qp];
                 } else {
-                  const double* nd = reinterpret_cast<const double*>(geo.data) + (i64)cellg * 81;
-                  double vx[3], dx[3], vy[3], dy[3], vz[3], dz[3], J[9];
+                  // J(xi_i, eta_j, zeta_k) from the column's pre-contracted node sums
+                  double J[9];
 #pragma unroll
-                  for (int c = 0; c < 3; ++c) {
-                    vx[c] = (double)gen.qv[i * 3 + c]; dx[c] = (double)gen.qd[i * 3 + c];
-                    vy[c] = (double)gen.qv[j * 3 + c]; dy[c] = (double)gen.qd[j * 3 + c];
-                    vz[c] = (double)gen.qv[k * 3 + c]; dz[c] = (double)gen.qd[k * 3 + c];
+                  for (int d = 0; d < 3; ++d) {
+                    double jx = 0.0, jy = 0.0, jz = 0.0;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                      const double vz = (double)gen.qv[k * 3 + c], dz = (double)gen.qd[k * 3 + c];
+                      jx += colx[c * 3 + d] * vz;
+                      jy += coly[c * 3 + d] * vz;
+                      jz += colv[c * 3 + d] * dz;
+                    }
+                    J[d * 3 + 0] = jx; J[d * 3 + 1] = jy; J[d * 3 + 2] = jz;
                   }
-                  jacobian27(nd, vx, dx, vy, dy, vz, dz, J);
                   const double det = invert3(J, inv);
                   jxw = det * (double)gen.w3[i] * (double)gen.w3[j] * (double)gen.w3[k];
                 }
