@@ -141,6 +141,19 @@ class Engine : public EngineBase {
     pack(M, tab_.Me, tab_.Mo);
     pack(K, tab_.Ke, tab_.Ko);
     for (int d = 0; d < 3; ++d) tab_.g[d] = (T)(det / (c_->h[d] * c_->h[d]));
+    // separable factors of the GL-collocation diagonal (index 0: sum over the two cells at a cell boundary)
+    for (int i = 0; i < P; ++i) {
+      double dd0 = 0.0, ddp = 0.0, ddi = 0.0;
+      for (int q = 0; q < N; ++q) {
+        dd0 += c_->glw[q] * c_->glD[q * N + 0] * c_->glD[q * N + 0];
+        ddp += c_->glw[q] * c_->glD[q * N + P] * c_->glD[q * N + P];
+        ddi += c_->glw[q] * c_->glD[q * N + i] * c_->glD[q * N + i];
+      }
+      tab_.wa[i] = i == 0 ? c_->glw[0] + c_->glw[P] : c_->glw[i];
+      tab_.da[i] = i == 0 ? dd0 + ddp : ddi;
+    }
+    tab_.wa[P] = tab_.da[P] = 0.0;
+    tab_.diag_onfly = 0;
     general_ = c_->geometry != MFCG_GEOM_AFFINE;
     if (general_) {
       if (c_->nq != N) {
@@ -560,6 +573,7 @@ class Engine : public EngineBase {
     event_cursor_ = 0;
     if ((rc = load_vec(a->b, a->location, r_))) return rc;
     const bool prec = a->variant == MFCG_COMBINED_PCG;
+    tab_.diag_onfly = (prec && !a->inv_diag && !general_) ? 1 : 0;
     if (prec) {
       if (a->inv_diag) {
         if ((rc = load_vec(a->inv_diag, a->location, minv_))) return rc;
@@ -860,6 +874,8 @@ int Engine<P, T>::solve(const mfcg_solve_args* a, mfcg_solve_result* res) {
 
   // right-hand side: merged variants start with r = b, the standard ones stage b in v
   if ((rc = load_vec(a->b, a->location, merged ? r_ : v_))) return rc;
+  // the operator's own Jacobi diagonal on an affine mesh is separable: interior DoFs compute it
+  tab_.diag_onfly = (merged && prec && !a->inv_diag && !general_ && a->fused) ? 1 : 0;
   if (prec) {
     if (a->inv_diag) {
       if ((rc = load_vec(a->inv_diag, a->location, minv_))) return rc;
