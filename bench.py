@@ -101,13 +101,13 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def build_problem(cells, p, deform=0.0):
+def build_problem(cells, p, deform=0.0, components=1):
     from paper_2205_08909_b200 import dofs, mesh as pmesh
     mesh = pmesh.build_cartesian_mesh(cells)
     if deform:
         mesh = pmesh.deform_mesh(mesh, deform)
-    h = dofs.distribute_dofs(mesh, p, 1, constrain_boundary=True)
-    plan = dofs.make_batches(mesh, dofs.batch_size(p, 1, 8), "morton")
+    h = dofs.distribute_dofs(mesh, p, components, constrain_boundary=True)
+    plan = dofs.make_batches(mesh, dofs.batch_size(p, components, 8), "morton")
     return mesh, h, plan
 
 
@@ -191,11 +191,11 @@ def workload_cells(args, n_gpus):
 
 def workload_config(args, n_gpus):
     cells = workload_cells(args, n_gpus)
-    n_dofs = int(np.prod([c * args.degree + 1 for c in cells]))
+    n_dofs = int(np.prod([c * args.degree + 1 for c in cells])) * args.components
     which = ("BASELINE configs[1] top rung" if n_gpus == 1 and not args.cells
              else ("BASELINE configs[4] weak scaling, 80^3 cells per GPU in z-slabs" if not args.cells
                    else "custom"))
-    return {"workload": f"Q{args.degree} Poisson, Cartesian {cells[0]}x{cells[1]}x{cells[2]} cells, "
+    return {"workload": f"Q{args.degree} {'Poisson' if args.components == 1 else '3-component Laplace (BP4 type)'}, Cartesian {cells[0]}x{cells[1]}x{cells[2]} cells, "
                         f"{n_dofs} DoFs, fp64, Jacobi, seeded uniform[-1,1] RHS, {args.iters} merged-CG "
                         f"iterations per step ({which})",
             "cells": list(cells), "degree": args.degree, "n_dofs": n_dofs, "iterations_per_step": args.iters,
@@ -308,6 +308,8 @@ def main():
     ap.add_argument("--geometry", default="affine",
                     choices=["affine", "final_tensor_load", "inverse_jacobian_load", "quadratic_compute"])
     ap.add_argument("--deform", type=float, default=0.0)
+    ap.add_argument("--components", type=int, default=1, choices=[1, 3],
+                    help="3: vector Laplacian of the BP4 type (SURVEY.md 8f row 3); single GPU only")
     ap.add_argument("--ref-cells", type=int, default=32)
     ap.add_argument("--ref-iters", type=int, default=60)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -335,8 +337,8 @@ def main():
     p = args.degree
     cells = workload_cells(args, 1)
     t_setup = time.perf_counter()
-    mesh, h, plan = build_problem(cells, p, args.deform)
-    op = MatrixFreeOperator(OperatorSpec("laplace", 1, p, p + 1, GeometryVariant(args.geometry)), mesh, h, plan,
+    mesh, h, plan = build_problem(cells, p, args.deform, args.components)
+    op = MatrixFreeOperator(OperatorSpec("laplace", args.components, p, p + 1, GeometryVariant(args.geometry)), mesh, h, plan,
                             device=local_rank, precision=args.precision, brick=tuple(args.brick))
     info = op.info()
     n = h.n_dofs
@@ -377,10 +379,12 @@ def main():
     # dominant kernel, timed per launch with CUDA events on the library stream
     rt = step_dev(timed=True)
     op_ms = rt.device_stats["operator_ms"] / max(rt.device_stats["operator_launches"], 1)
-    n_int, n_sh = info["n_interior"], n - info["n_interior"]
+    nc = args.components                        # one brick-kernel launch per component field
+    n_int, n_sh = info["n_interior"], n // nc - info["n_interior"]
     w = 8 if args.precision == "fp64" else 4
     kernel_bytes = 8 * w * n_int + 2 * w * n_sh  # interior: the full 8 scalars; shared: read p, add to v
     kernel_bytes += info["geometry_bytes"]      # stored geometry streamed once per operator application
+    kernel_bytes *= nc
     peak, peak_src = measured_peak()
     achieved = kernel_bytes / (op_ms * 1e-3) / 1e9
     it_ms = rt.device_stats["solve_ms"] / args.iters
@@ -389,7 +393,7 @@ def main():
         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
         "traffic": None, "algorithmic_bytes_per_launch": kernel_bytes, "kernel_ms": op_ms,
         "iteration_ms": it_ms, "kernel_share_of_step": op_ms / it_ms,
-        "iteration_frac": (8 * w * n + info["geometry_bytes"]) / (it_ms * 1e-3) / 1e9 / peak,
+        "iteration_frac": (8 * w * n + nc * info["geometry_bytes"]) / (it_ms * 1e-3) / 1e9 / peak,
         "whole_solve_frac": value * 8 * w / 1e9 / peak,
     }
     prof = ROOT / "profiles" / "traffic.json"
@@ -398,7 +402,7 @@ def main():
             # ncu capture is taken at 73^3 cells (same kernel, same brick shape); DRAM bytes per DoF
             # are size independent above L2, so the per-launch figure is scaled to this workload
             tj = json.loads(prof.read_text())
-            if args.geometry == "affine" and args.degree == 5 and args.precision == "fp64":
+            if args.geometry == "affine" and args.degree == 5 and args.precision == "fp64" and nc == 1:
                 roofline["traffic"] = tj["bytes_per_dof"] * n
                 roofline["traffic_source"] = "profiles/traffic.json: " + tj["source"] + f"; {tj['workload']}, scaled by n_dofs"
         except Exception:

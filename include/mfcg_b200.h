@@ -93,6 +93,10 @@ typedef struct mfcg_op_desc {
   int32_t slab_z0;                /* first global cell layer of this slab                 */
   int32_t global_cells_z;         /* cell layers of the whole mesh (0: cells[2]); with    */
                                   /* slabs, `cells` is the slab and `extents` the mesh    */
+  int32_t components;             /* OperatorSpec.components: 1 or 3 (0 reads as 1); with 3, */
+                                  /* vectors interleave the components of a node             */
+                                  /* (dofs.py:229-236), n_dofs = 3 * nodes and `constrained` */
+                                  /* lists whole nodes; the diagonal stays one value per node */
 } mfcg_op_desc;
 
 int mfcg_op_create(mfcg_ctx* ctx, const mfcg_op_desc* desc, mfcg_op** op);
@@ -113,11 +117,13 @@ int mfcg_op_get_info(mfcg_op* op, mfcg_op_info* info);
 int mfcg_op_device_permutation(mfcg_op* op, int32_t* perm_host);
 
 /* dst = A src; replaces MatrixFreeOperator.apply (operator.py:285-292).
- * src/dst: fp64[n_dofs], caller numbering; location 0 host / 1 device. */
+ * src/dst: fp64[n_dofs], caller numbering; location 0 host / 1 device.
+ * With 3 components the scalar operator acts on each component (operator.py:256-281). */
 int mfcg_op_apply(mfcg_op* op, const double* src, double* dst, int location);
 
 /* 1/diag of the GL-collocation operator, constrained entries 1; replaces
  * MatrixFreeOperator.compute_diagonal (operator.py:380-418).
+ * inv_diag: fp64[n_dofs / components] (one value per node, operator.py:90).
  * Returns MFCG_EINVAL "operator diagonal is not positive definite" like :416-417. */
 int mfcg_op_diagonal(mfcg_op* op, double* inv_diag, int location);
 
@@ -131,7 +137,7 @@ typedef struct mfcg_solve_args {
   int32_t variant;            /* MFCG_CG ...                                         */
   int32_t location;           /* of b, inv_diag, x: 0 host, 1 device                 */
   const double* b;            /* right-hand side [n_dofs]                            */
-  const double* inv_diag;     /* scalar inverse diagonal [n_dofs] or NULL            */
+  const double* inv_diag;     /* scalar inverse diagonal [n_dofs / components] or NULL */
   double* x;                  /* out: solution [n_dofs]                              */
   double tolerance;           /* SolverConfig.tolerance      solvers.py:41           */
   int32_t max_iterations;     /* SolverConfig.max_iterations                         */

@@ -24,15 +24,15 @@ OUT.mkdir(parents=True, exist_ok=True)
 
 
 def build(cells, p, nq, *, constrain=True, numbering="default", traversal="morton", batch=None,
-          deform=0.0, variant=GeometryVariant.AFFINE, quadrature="gauss"):
+          deform=0.0, variant=GeometryVariant.AFFINE, quadrature="gauss", components=1):
     mesh = build_cartesian_mesh(cells)
     if deform:
         mesh = deform_mesh(mesh, deform)
-    h = distribute_dofs(mesh, p, 1, constrain_boundary=constrain)
-    plan = make_batches(mesh, batch or batch_size(p, 1, 8), traversal)
+    h = distribute_dofs(mesh, p, components, constrain_boundary=constrain)
+    plan = make_batches(mesh, batch or batch_size(p, components, 8), traversal)
     if numbering == "optimized":
         h = renumber_optimized(h, plan)
-    spec = OperatorSpec("laplace", 1, p, nq, variant, quadrature)
+    spec = OperatorSpec("laplace", components, p, nq, variant, quadrature)
     return MatrixFreeOperator(spec, mesh, h, plan), h, plan, mesh
 
 
@@ -194,10 +194,49 @@ def curved():
 
 
 def harness_rhs():
-    """Manufactured right-hand side of BP5, p = 3, (3,2,2) cells, deformation 0.05."""
+    """Manufactured right-hand sides: BP5 and BP4 (3 components), p = 3, (3,2,2) cells,
+    deformation 0.05."""
     from mfcg.bench import assemble_problem
     _, b, _ = assemble_problem("BP5", 3, (3, 2, 2))
-    np.savez_compressed(OUT / "harness.npz", bp5_p3_322_rhs=b)
+    _, b4, _ = assemble_problem("BP4", 3, (3, 2, 2))
+    np.savez_compressed(OUT / "harness.npz", bp5_p3_322_rhs=b, bp4_p3_322_rhs=b4)
+
+
+# (cells, p, nq, numbering, deformation, geometry variant): 3-component Laplace (BP4-type)
+VECTOR_CASES = [((3, 2, 2), 2, 3, "default", 0.0, "affine"),
+                ((4, 4, 4), 5, 6, "optimized", 0.0, "affine"),
+                ((3, 3, 3), 3, 4, "default", 0.1, "final_tensor_load"),
+                ((5, 4, 3), 4, 5, "default", 0.0, "affine")]
+
+
+def vector3():
+    out = {}
+    for ci, (cells, p, nq, numbering, amp, variant) in enumerate(VECTOR_CASES):
+        op, h, plan, mesh = build(cells, p, nq, numbering=numbering, deform=amp,
+                                  variant=GeometryVariant(variant), components=3)
+        rng = np.random.default_rng(300 + ci)
+        u = rng.standard_normal(h.n_dofs)
+        out[f"v{ci}_blocks"] = h.cell_index_blocks
+        out[f"v{ci}_constrained"] = h.constrained_dofs
+        if h.permutation is not None:
+            out[f"v{ci}_permutation"] = h.permutation
+        out[f"v{ci}_u"] = u
+        out[f"v{ci}_Au"] = op.apply(u)
+        minv = op.compute_diagonal()
+        out[f"v{ci}_invdiag"] = minv.inverse_diagonal
+        b = np.random.default_rng(0).uniform(-1.0, 1.0, h.n_dofs)
+        if h.permutation is not None:
+            bo = np.empty_like(b)
+            bo[h.permutation] = b
+            b = bo
+        b[h.constrained_dofs] = 0.0
+        out[f"v{ci}_b"] = b
+        for variant_name in ("pcg", "combined_pcg", "combined_cg"):
+            res = solve(variant_name, op, b, minv=None if variant_name == "combined_cg" else minv,
+                        config=SolverConfig(fixed_iterations=30))
+            out[f"v{ci}_{variant_name}_hist"] = hist_array(res)
+            out[f"v{ci}_{variant_name}_x"] = res.x
+    np.savez_compressed(OUT / "vector3.npz", **out)
 
 
 if __name__ == "__main__":
@@ -208,5 +247,6 @@ if __name__ == "__main__":
     config1()
     q5_small()
     curved()
+    vector3()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)

@@ -35,7 +35,7 @@ class OpDesc(C.Structure):
         ("cell_index_blocks", C.POINTER(C.c_int32)), ("n_dofs", C.c_int64),
         ("constrained", C.POINTER(C.c_int64)), ("n_constrained", C.c_int64),
         ("geometry", C.c_int32), ("precision", C.c_int32), ("brick", C.c_int32 * 3),
-        ("slab_z0", C.c_int32), ("global_cells_z", C.c_int32),
+        ("slab_z0", C.c_int32), ("global_cells_z", C.c_int32), ("components", C.c_int32),
     ]
 
 

@@ -186,11 +186,18 @@ static int op_create_impl(mfcg_ctx* ctx, const mfcg_op_desc* d, mfcg_op* op) {
   if (d->geometry < 0 || d->geometry > 3) { set_error("unknown geometry variant"); return MFCG_EINVAL; }
   if (d->precision != 0 && d->precision != 1) { set_error("precision must be 0 (fp64) or 1 (fp32)"); return MFCG_EINVAL; }
   const i64 NX = (i64)d->cells[0] * p + 1, NY = (i64)d->cells[1] * p + 1, NZ = (i64)d->cells[2] * p + 1;
-  if (d->n_dofs != NX * NY * NZ) {
-    set_error("vector length does not match handler");  // scalar problems only
+  const int C = d->components == 0 ? 1 : d->components;
+  if (C != 1 && C != 3) { set_error("components must be 1 or 3"); return MFCG_EINVAL; }  // operator.py:65-66
+  if (d->n_dofs != NX * NY * NZ * C) {
+    set_error("vector length does not match handler");
     return MFCG_EINVAL;
   }
-  if (d->n_dofs >= (i64)2147483647) { set_error("more than 2^31-1 DoFs per GPU are not supported"); return MFCG_EUNSUPPORTED; }
+  if (C > 1 && (d->slab_z0 != 0 || (d->global_cells_z > 0 && d->global_cells_z != d->cells[2]))) {
+    set_error("z-slabs of a 3-component operator are not supported");
+    return MFCG_EUNSUPPORTED;
+  }
+  c.ncomp = C;
+  if (d->n_dofs / C >= (i64)2147483647) { set_error("more than 2^31-1 DoFs per GPU are not supported"); return MFCG_EUNSUPPORTED; }
   c.p = p;
   c.nq = nq;
   c.precision = d->precision;
@@ -206,7 +213,7 @@ static int op_create_impl(mfcg_ctx* ctx, const mfcg_op_desc* d, mfcg_op* op) {
   c.glD.assign(d->gl_gradients, d->gl_gradients + (p + 1) * (p + 1));
   BrickGrid& g = c.grid;
   g.p = p;
-  g.n_dofs = d->n_dofs;
+  g.n_dofs = d->n_dofs / C;  // lattice nodes; every component is one scalar field of this length
   // z-slab: `cells` are this slab's cells, `extents` those of the whole mesh
   c.global_cells_z = d->global_cells_z > 0 ? d->global_cells_z : d->cells[2];
   c.slab_z0 = d->slab_z0;
@@ -288,7 +295,7 @@ static int op_create_impl(mfcg_ctx* ctx, const mfcg_op_desc* d, mfcg_op* op) {
   g.mask = c.d_mask;
   MFCG_CUDA(cudaMalloc(&c.d_perm, sizeof(int) * g.n_dofs));
   MFCG_CUDA(cudaMemsetAsync(c.d_perm, 0xff, sizeof(int) * g.n_dofs, st));
-  MFCG_CUDA(cudaMalloc(&c.d_io, sizeof(double) * g.n_dofs));
+  MFCG_CUDA(cudaMalloc(&c.d_io, sizeof(double) * g.n_dofs * C));
   MFCG_CUDA(cudaMalloc(&c.d_state, sizeof(SolveState)));
   MFCG_CUDA(cudaMallocHost(&c.h_state, sizeof(SolveState)));
   MFCG_CUDA(cudaMalloc(&c.d_flag, sizeof(int)));
@@ -306,10 +313,18 @@ static int op_create_impl(mfcg_ctx* ctx, const mfcg_op_desc* d, mfcg_op* op) {
   }
   if (d->n_constrained > 0) {
     if (!d->constrained) { set_error("constrained list is NULL"); return MFCG_EINVAL; }
+    if (C > 1) {  // dofs.py:174-178, 329-330: constraints cover whole nodes (all components)
+      std::vector<i64> con(d->constrained, d->constrained + d->n_constrained);
+      std::sort(con.begin(), con.end());
+      bool whole = con.size() % C == 0;
+      for (size_t t = 0; whole && t < con.size(); t += C)
+        for (int j = 0; j < C; ++j) whole = whole && con[t + j] == con[t] + j && con[t] % C == 0;
+      if (!whole) { set_error("constraints must cover whole nodes (all components)"); return MFCG_EINVAL; }
+    }
     i64* d_con = nullptr;
     MFCG_CUDA(cudaMalloc(&d_con, sizeof(i64) * d->n_constrained));
     MFCG_CUDA(cudaMemcpyAsync(d_con, d->constrained, sizeof(i64) * d->n_constrained, cudaMemcpyHostToDevice, st));
-    k_mark_constrained<<<vgrid, 256, 0, st>>>(d->n_constrained, d_con, c.d_perm, g.n_int, c.d_mask, c.d_flag);
+    k_mark_constrained<<<vgrid, 256, 0, st>>>(d->n_constrained, C, d_con, c.d_perm, g.n_int, c.d_mask, c.d_flag);
     MFCG_CUDA(cudaGetLastError());
     int flag = 0;
     MFCG_CUDA(cudaMemcpyAsync(&flag, c.d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));

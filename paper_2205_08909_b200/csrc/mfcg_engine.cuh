@@ -39,6 +39,7 @@ struct OpCommon {
   BrickGrid grid{};
   i64 n_cells = 0;
   int p = 1, nq = 2, precision = 0, geometry = 0;
+  int ncomp = 1;  // vector components per node (1 or 3); grid.n_dofs counts nodes
   std::vector<double> S, D, xq, wq, glx, glw, glD;
   double extents[3] = {1, 1, 1}, h[3] = {1, 1, 1}, deformation = 0.0;
   i64 n_bricks = 0;
@@ -173,7 +174,12 @@ class Engine : public EngineBase {
       MFCG_CUDA(cudaFuncSetAttribute(k_brick<P, T, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
     }
     vgrid_ = c_->ctx->sm_count * 8;
-    const i64 rows = c_->n_bricks + vgrid_;
+    // one scalar field per component, fields 256-byte aligned; the gaps stay zero
+    C_ = c_->ncomp;
+    cs_ = C_ == 1 ? c_->grid.n_dofs : (c_->grid.n_dofs + 31) / 32 * 32;
+    nt_ = cs_ * C_;
+    rows_pc_ = c_->n_bricks + vgrid_;
+    const i64 rows = rows_pc_ * C_;
     MFCG_CUDA(cudaMalloc(&partials_a_, sizeof(double) * 8 * rows));
     MFCG_CUDA(cudaMalloc(&partials_b_, sizeof(double) * 8 * rows));
     MFCG_CUDA(cudaMemsetAsync(partials_a_, 0, sizeof(double) * 8 * rows, stream()));
@@ -182,7 +188,7 @@ class Engine : public EngineBase {
   }
 
   void info(mfcg_op_info* out) override {
-    out->n_dofs = c_->grid.n_dofs;
+    out->n_dofs = c_->grid.n_dofs * C_;
     out->n_interior = c_->grid.n_int;
     out->n_bricks = c_->n_bricks;
     for (int d = 0; d < 3; ++d) out->brick[d] = c_->grid.B[d];
@@ -206,7 +212,7 @@ class Engine : public EngineBase {
     if (rc) return rc;
     const i64 n = c_->grid.n_dofs;
     double* target = location ? out : c_->d_io;
-    k_to_user_order<double><<<vgrid_, VT, 0, stream()>>>(n, c_->d_perm, c_->d_invdiag, target);
+    k_to_user_order<double><<<vgrid_, VT, 0, stream()>>>(n, 1, n, c_->d_perm, c_->d_invdiag, target);
     MFCG_CUDA(cudaGetLastError());
     if (!location) MFCG_CUDA(cudaMemcpyAsync(out, c_->d_io, sizeof(double) * n, cudaMemcpyDeviceToHost, stream()));
     MFCG_CUDA(cudaStreamSynchronize(stream()));
@@ -239,11 +245,16 @@ class Engine : public EngineBase {
   cudaStream_t stream() const { return c_->ctx->stream; }
 
   int ensure_vectors(bool all) {
-    const i64 n = c_->grid.n_dofs;
     // +32 bytes: the brick kernel reads whole aligned 16-byte chunks
-    for (T** v : {&p_, &v_}) if (!*v) MFCG_CUDA(cudaMalloc(v, sizeof(T) * n + 32));
+    auto need = [&](T** v) -> int {
+      if (*v) return MFCG_OK;
+      MFCG_CUDA(cudaMalloc(v, sizeof(T) * nt_ + 32));
+      if (C_ > 1) MFCG_CUDA(cudaMemsetAsync(*v, 0, sizeof(T) * nt_ + 32, stream()));
+      return MFCG_OK;
+    };
+    for (T** v : {&p_, &v_}) if (int rc = need(v)) return rc;
     if (all)
-      for (T** v : {&x_, &r_, &z_, &minv_}) if (!*v) MFCG_CUDA(cudaMalloc(v, sizeof(T) * n + 32));
+      for (T** v : {&x_, &r_, &z_, &minv_}) if (int rc = need(v)) return rc;
     return MFCG_OK;
   }
 
@@ -308,14 +319,16 @@ class Engine : public EngineBase {
   }
 
   // caller numbering (fp64, host or device) -> brick numbering (T, device)
-  int load_vec(const double* usr, int location, T* dev) {
+  // `usr_comp` == 1: a per-node scalar replicated into every component field
+  int load_vec(const double* usr, int location, T* dev, int usr_comp = 0) {
     const i64 n = c_->grid.n_dofs;
+    if (usr_comp == 0) usr_comp = C_;
     const double* from = usr;
     if (!location) {
-      MFCG_CUDA(cudaMemcpyAsync(c_->d_io, usr, sizeof(double) * n, cudaMemcpyHostToDevice, stream()));
+      MFCG_CUDA(cudaMemcpyAsync(c_->d_io, usr, sizeof(double) * n * usr_comp, cudaMemcpyHostToDevice, stream()));
       from = c_->d_io;
     }
-    k_to_device_order<T><<<vgrid_, VT, 0, stream()>>>(n, c_->d_perm, from, dev);
+    k_to_device_order<T><<<vgrid_, VT, 0, stream()>>>(n, C_, cs_, usr_comp, c_->d_perm, from, dev);
     MFCG_CUDA(cudaGetLastError());
     ++launches_;
     return MFCG_OK;
@@ -324,10 +337,10 @@ class Engine : public EngineBase {
   int store_vec(const T* dev, double* usr, int location) {
     const i64 n = c_->grid.n_dofs;
     double* target = location ? usr : c_->d_io;
-    k_to_user_order<T><<<vgrid_, VT, 0, stream()>>>(n, c_->d_perm, dev, target);
+    k_to_user_order<T><<<vgrid_, VT, 0, stream()>>>(n, C_, cs_, c_->d_perm, dev, target);
     MFCG_CUDA(cudaGetLastError());
     ++launches_;
-    if (!location) MFCG_CUDA(cudaMemcpyAsync(usr, c_->d_io, sizeof(double) * n, cudaMemcpyDeviceToHost, stream()));
+    if (!location) MFCG_CUDA(cudaMemcpyAsync(usr, c_->d_io, sizeof(double) * n * C_, cudaMemcpyDeviceToHost, stream()));
     return MFCG_OK;
   }
 
@@ -348,27 +361,35 @@ class Engine : public EngineBase {
     }
     const unsigned nb = (unsigned)count;
     const int off = (int)first;
-    if (!general_) {
-      if (mode == 0)
-        k_brick<P, T, 0, 0><<<nb, Cfg<P, 0>::THREADS, smem_, stream()>>>(
-            c_->grid, tab_, gen_, geo_, src, nullptr, v, nullptr, nullptr, nullptr, nullptr, nullptr, off);
-      else
-        k_brick<P, T, 1, 0><<<nb, Cfg<P, 0>::THREADS, smem_, stream()>>>(
-            c_->grid, tab_, gen_, geo_, nullptr, pv, v, r_, x_, minv_, c_->d_state, partials, off);
-    } else if (c_->geometry != MFCG_GEOM_QUADRATIC_COMPUTE) {
-      if (mode == 0)
-        k_brick<P, T, 0, 1><<<nb, Cfg<P, 1>::THREADS, smem_, stream()>>>(
-            c_->grid, tab_, gen_, geo_, src, nullptr, v, nullptr, nullptr, nullptr, nullptr, nullptr, off);
-      else
-        k_brick<P, T, 1, 1><<<nb, Cfg<P, 1>::THREADS, smem_, stream()>>>(
-            c_->grid, tab_, gen_, geo_, nullptr, pv, v, r_, x_, minv_, c_->d_state, partials, off);
-    } else {
-      if (mode == 0)
-        k_brick<P, T, 0, 2><<<nb, Cfg<P, 2>::THREADS, smem_, stream()>>>(
-            c_->grid, tab_, gen_, geo_, src, nullptr, v, nullptr, nullptr, nullptr, nullptr, nullptr, off);
-      else
-        k_brick<P, T, 1, 2><<<nb, Cfg<P, 2>::THREADS, smem_, stream()>>>(
-            c_->grid, tab_, gen_, geo_, nullptr, pv, v, r_, x_, minv_, c_->d_state, partials, off);
+    for (int comp = 0; comp < C_; ++comp) {
+      const i64 o = comp * cs_;
+      const T* s_ = src ? src + o : nullptr;
+      T* pv_ = pv ? pv + o : nullptr;
+      T* vv_ = v + o;
+      T *rr_ = r_ ? r_ + o : nullptr, *xx_ = x_ ? x_ + o : nullptr, *mm_ = minv_ ? minv_ + o : nullptr;
+      double* part_ = partials ? partials + 8 * comp * rows_pc_ : nullptr;
+      if (!general_) {
+        if (mode == 0)
+          k_brick<P, T, 0, 0><<<nb, Cfg<P, 0>::THREADS, smem_, stream()>>>(
+              c_->grid, tab_, gen_, geo_, s_, nullptr, vv_, nullptr, nullptr, nullptr, nullptr, nullptr, off);
+        else
+          k_brick<P, T, 1, 0><<<nb, Cfg<P, 0>::THREADS, smem_, stream()>>>(
+              c_->grid, tab_, gen_, geo_, nullptr, pv_, vv_, rr_, xx_, mm_, c_->d_state, part_, off);
+      } else if (c_->geometry != MFCG_GEOM_QUADRATIC_COMPUTE) {
+        if (mode == 0)
+          k_brick<P, T, 0, 1><<<nb, Cfg<P, 1>::THREADS, smem_, stream()>>>(
+              c_->grid, tab_, gen_, geo_, s_, nullptr, vv_, nullptr, nullptr, nullptr, nullptr, nullptr, off);
+        else
+          k_brick<P, T, 1, 1><<<nb, Cfg<P, 1>::THREADS, smem_, stream()>>>(
+              c_->grid, tab_, gen_, geo_, nullptr, pv_, vv_, rr_, xx_, mm_, c_->d_state, part_, off);
+      } else {
+        if (mode == 0)
+          k_brick<P, T, 0, 2><<<nb, Cfg<P, 2>::THREADS, smem_, stream()>>>(
+              c_->grid, tab_, gen_, geo_, s_, nullptr, vv_, nullptr, nullptr, nullptr, nullptr, nullptr, off);
+        else
+          k_brick<P, T, 1, 2><<<nb, Cfg<P, 2>::THREADS, smem_, stream()>>>(
+              c_->grid, tab_, gen_, geo_, nullptr, pv_, vv_, rr_, xx_, mm_, c_->d_state, part_, off);
+      }
     }
     MFCG_CUDA(cudaGetLastError());
     if (time_kernels_) MFCG_CUDA(cudaEventRecord(e1, stream()));
@@ -381,16 +402,17 @@ class Engine : public EngineBase {
   int launch_apply(const T* src, T* dst) {
     const bool has_shared = c_->grid.n_dofs > c_->grid.n_int;
     if (has_shared) {
-      k_surface_init<T><<<vgrid_, VT, 0, stream()>>>(c_->grid, dst);
+      for (int comp = 0; comp < C_; ++comp) k_surface_init<T><<<vgrid_, VT, 0, stream()>>>(c_->grid, dst + comp * cs_);
       MFCG_CUDA(cudaGetLastError());
-      ++launches_;
+      launches_ += C_;
     }
     int rc = launch_brick(0, src, nullptr, dst, nullptr);
     if (rc) return rc;
     if (has_shared) {
-      k_surface_fix<T><<<vgrid_, VT, 0, stream()>>>(c_->grid, src, dst);
+      for (int comp = 0; comp < C_; ++comp)
+        k_surface_fix<T><<<vgrid_, VT, 0, stream()>>>(c_->grid, src + comp * cs_, dst + comp * cs_);
       MFCG_CUDA(cudaGetLastError());
-      ++launches_;
+      launches_ += C_;
     }
     return MFCG_OK;
   }
@@ -615,7 +637,7 @@ class Engine : public EngineBase {
   int g_end(const mfcg_solve_args* a, mfcg_solve_result* res) override {
     std::memset(res, 0, sizeof(*res));
     const i64 n = c_->grid.n_dofs;
-    k_finalize_x<T><<<vgrid_, VT, 0, stream()>>>(n, x_, p_, r_, minv_, c_->d_state);
+    k_finalize_x<T><<<vgrid_, VT, 0, stream()>>>(nt_, x_, p_, r_, minv_, c_->d_state);
     ++launches_;
     int rc = store_vec(x_, a->x, a->location);
     if (rc) return rc;
@@ -752,6 +774,8 @@ class Engine : public EngineBase {
   double* diag_raw_ = nullptr;  // slab runs: diagonal before the interface exchange
   cudaEvent_t ev_front_ = nullptr;
   int smem_ = 0, vgrid_ = 0;
+  int C_ = 1;                         // components
+  i64 cs_ = 0, nt_ = 0, rows_pc_ = 0;  // component stride, device vector length, partial rows per component
   T *x_ = nullptr, *r_ = nullptr, *p_ = nullptr, *v_ = nullptr, *z_ = nullptr, *minv_ = nullptr;
   double *partials_a_ = nullptr, *partials_b_ = nullptr, *d_history_ = nullptr;
   int history_cap_ = 0;
@@ -766,30 +790,44 @@ int Engine<P, T>::run_merged(const mfcg_solve_args* a, int limit) {
   const BrickGrid& g = c_->grid;
   const i64 n = g.n_dofs, n_sh = g.n_dofs - g.n_int;
   const bool fixed = a->fixed_iterations >= 0;
-  const int rows_fused = (int)c_->n_bricks + (n_sh > 0 ? vgrid_ : 0);
+  // rows of partial sums: per component, one per brick and one per k_post block (unused rows stay zero)
+  const int rows_fused = (int)(rows_pc_ * C_);
   for (int it = 1; it <= limit; ++it) {
     if (a->fused) {
       if (n_sh > 0) {
-        k_pre<T><<<vgrid_, VT, 0, stream()>>>(g, g.n_int, n, 1, r_, p_, v_, x_, minv_, c_->d_state);
-        ++launches_;
+        for (int c = 0; c < C_; ++c) {
+          const i64 o = c * cs_;
+          k_pre<T><<<vgrid_, VT, 0, stream()>>>(g, g.n_int, n, 1, r_ + o, p_ + o, v_ + o, x_ + o, minv_ + o, c_->d_state);
+        }
+        launches_ += C_;
       }
       int rc = launch_brick(1, nullptr, p_, v_, partials_a_);
       if (rc) return rc;
       if (n_sh > 0) {
-        k_post<T><<<vgrid_, VT, 0, stream()>>>(g, g.n_int, n, 1, r_, p_, v_, minv_, c_->d_state,
-                                               partials_a_ + 8 * c_->n_bricks);
-        ++launches_;
+        for (int c = 0; c < C_; ++c) {
+          const i64 o = c * cs_;
+          k_post<T><<<vgrid_, VT, 0, stream()>>>(g, g.n_int, n, 1, r_ + o, p_ + o, v_ + o, minv_ + o, c_->d_state,
+                                                 partials_a_ + 8 * (c * rows_pc_ + c_->n_bricks));
+        }
+        launches_ += C_;
       }
       k_scalar_merged<<<1, 256, 0, stream()>>>(partials_a_, rows_fused, c_->d_state, d_history_);
       ++launches_;
     } else {
       // the paper's GPU scheme: pre, mat-vec and post as separate kernels
-      k_pre<T><<<vgrid_, VT, 0, stream()>>>(g, 0, n, 0, r_, p_, v_, x_, minv_, c_->d_state);
+      for (int c = 0; c < C_; ++c) {
+        const i64 o = c * cs_;
+        k_pre<T><<<vgrid_, VT, 0, stream()>>>(g, 0, n, 0, r_ + o, p_ + o, v_ + o, x_ + o, minv_ + o, c_->d_state);
+      }
       int rc = launch_apply(p_, v_);
       if (rc) return rc;
-      k_post<T><<<vgrid_, VT, 0, stream()>>>(g, 0, n, 0, r_, p_, v_, minv_, c_->d_state, partials_a_);
-      k_scalar_merged<<<1, 256, 0, stream()>>>(partials_a_, vgrid_, c_->d_state, d_history_);
-      launches_ += 3;
+      for (int c = 0; c < C_; ++c) {
+        const i64 o = c * cs_;
+        k_post<T><<<vgrid_, VT, 0, stream()>>>(g, 0, n, 0, r_ + o, p_ + o, v_ + o, minv_ + o, c_->d_state,
+                                               partials_a_ + 8 * c * vgrid_);
+      }
+      k_scalar_merged<<<1, 256, 0, stream()>>>(partials_a_, vgrid_ * C_, c_->d_state, d_history_);
+      launches_ += 2 * C_ + 1;
     }
     MFCG_CUDA(cudaGetLastError());
     if (!fixed && (it % 16 == 0)) {
@@ -798,7 +836,7 @@ int Engine<P, T>::run_merged(const mfcg_solve_args* a, int limit) {
       if (!c_->h_state->active) break;
     }
   }
-  k_finalize_x<T><<<vgrid_, VT, 0, stream()>>>(n, x_, p_, r_, minv_, c_->d_state);
+  k_finalize_x<T><<<vgrid_, VT, 0, stream()>>>(nt_, x_, p_, r_, minv_, c_->d_state);
   MFCG_CUDA(cudaGetLastError());
   ++launches_;
   return MFCG_OK;
@@ -807,7 +845,7 @@ int Engine<P, T>::run_merged(const mfcg_solve_args* a, int limit) {
 template <int P, typename T>
 int Engine<P, T>::run_standard(const mfcg_solve_args* a, int limit, bool prec) {
   const BrickGrid& g = c_->grid;
-  const i64 n = g.n_dofs;
+  const i64 n = nt_;  // flat over all component fields
   const bool fixed = a->fixed_iterations >= 0;
   T* z = prec ? z_ : r_;
   // v_ holds b in brick numbering on entry
@@ -846,7 +884,7 @@ template <int P, typename T>
 int Engine<P, T>::solve(const mfcg_solve_args* a, mfcg_solve_result* res) {
   std::memset(res, 0, sizeof(*res));
   const BrickGrid& g = c_->grid;
-  const i64 n = g.n_dofs;
+  const i64 n = nt_;  // flat over all component fields (gaps between fields are zero)
   const bool merged = a->variant == MFCG_COMBINED_CG || a->variant == MFCG_COMBINED_PCG;
   const bool prec = a->variant == MFCG_PCG || a->variant == MFCG_COMBINED_PCG;
   if (a->variant < 0 || a->variant > 3) { set_error("unknown solver variant"); return MFCG_EINVAL; }
@@ -878,11 +916,12 @@ int Engine<P, T>::solve(const mfcg_solve_args* a, mfcg_solve_result* res) {
   tab_.diag_onfly = (merged && prec && !a->inv_diag && !general_ && a->fused) ? 1 : 0;
   if (prec) {
     if (a->inv_diag) {
-      if ((rc = load_vec(a->inv_diag, a->location, minv_))) return rc;
+      if ((rc = load_vec(a->inv_diag, a->location, minv_, 1))) return rc;
     } else {
       if ((rc = ensure_diagonal())) return rc;
-      k_convert<T, double><<<vgrid_, VT, 0, stream()>>>(n, c_->d_invdiag, minv_);
-      ++launches_;
+      for (int c = 0; c < C_; ++c)
+        k_convert<T, double><<<vgrid_, VT, 0, stream()>>>(g.n_dofs, c_->d_invdiag, minv_ + c * cs_);
+      launches_ += C_;
     }
   } else if (merged) {
     k_fill<T><<<vgrid_, VT, 0, stream()>>>(n, minv_, (T)1);

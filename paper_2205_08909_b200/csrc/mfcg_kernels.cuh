@@ -1461,24 +1461,37 @@ static __global__ void k_build_perm(BrickGrid g, const int* __restrict__ blocks,
   }
 }
 
-// dev[perm[u]] = (T) usr[u]
+// Caller numbering -> brick numbering.  The caller interleaves the components of a node
+// (dofs.py:229-236: index = node * C + c); the device keeps one scalar field per component,
+// dev[c * cs + perm[node]] (cs >= n: component stride).  `usr_comp` == 1 replicates a per-node scalar (the Jacobi diagonal,
+// operator.py:92-94) into all C fields.
 template <typename T>
-__global__ void k_to_device_order(i64 n, const int* __restrict__ perm, const double* __restrict__ usr, T* __restrict__ dev) {
-  for (i64 u = blockIdx.x * (i64)blockDim.x + threadIdx.x; u < n; u += (i64)gridDim.x * blockDim.x)
-    dev[perm[u]] = (T)usr[u];
+__global__ void k_to_device_order(i64 n, int C, i64 cs, int usr_comp, const int* __restrict__ perm,
+                                  const double* __restrict__ usr, T* __restrict__ dev) {
+  const i64 total = n * C;
+  for (i64 u = blockIdx.x * (i64)blockDim.x + threadIdx.x; u < total; u += (i64)gridDim.x * blockDim.x) {
+    const i64 node = u / C;
+    const int c = (int)(u - node * C);
+    dev[c * cs + perm[node]] = (T)(usr_comp == 1 ? usr[node] : usr[u]);
+  }
 }
 
-// usr[u] = (double) dev[perm[u]]
+// usr[node * C + c] = (double) dev[c * cs + perm[node]]
 template <typename T>
-__global__ void k_to_user_order(i64 n, const int* __restrict__ perm, const T* __restrict__ dev, double* __restrict__ usr) {
-  for (i64 u = blockIdx.x * (i64)blockDim.x + threadIdx.x; u < n; u += (i64)gridDim.x * blockDim.x)
-    usr[u] = (double)dev[perm[u]];
+__global__ void k_to_user_order(i64 n, int C, i64 cs, const int* __restrict__ perm, const T* __restrict__ dev,
+                                double* __restrict__ usr) {
+  const i64 total = n * C;
+  for (i64 u = blockIdx.x * (i64)blockDim.x + threadIdx.x; u < total; u += (i64)gridDim.x * blockDim.x) {
+    const i64 node = u / C;
+    const int c = (int)(u - node * C);
+    usr[u] = (double)dev[c * cs + perm[node]];
+  }
 }
 
-static __global__ void k_mark_constrained(i64 k, const i64* __restrict__ constrained, const int* __restrict__ perm,
+static __global__ void k_mark_constrained(i64 k, int C, const i64* __restrict__ constrained, const int* __restrict__ perm,
                                    i64 n_int, unsigned char* __restrict__ mask, int* __restrict__ error) {
   for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < k; t += (i64)gridDim.x * blockDim.x) {
-    const i64 d = perm[constrained[t]];
+    const i64 d = perm[constrained[t] / C];
     if (d < n_int) *error = 1;  // a constrained DoF strictly inside a brick: not a boundary constraint
     else mask[d - n_int] |= 1;
   }

@@ -9,7 +9,8 @@ device-resident operator in ``libmfcg_b200.so``: ``apply`` and
 whole CG loop to the library.  The hot path has no CPU implementation here:
 without the library or a GPU the constructor raises.
 
-Scope: scalar Laplace; ``components == 3`` and the mass
+Scope: the Laplace operator on 1 or 3 components (the
+scalar operator acts on every component, operator.py:256-281); the mass
 equations are rejected with ``NotImplementedError``.
 """
 
@@ -103,10 +104,12 @@ class MatrixFreeOperator:
             raise ValueError("spec/handler degree mismatch")
         if tuple(mesh.cells_per_dim) != tuple(handler.cells_per_dim):
             raise ValueError("mesh/handler shape mismatch")
-        if spec.equation != "laplace" or spec.components != 1:
+        if spec.equation != "laplace":
             raise NotImplementedError(
-                "the B200 hot path covers the scalar Laplace operator (SURVEY.md section 8); "
-                "mass equations and 3-component vectors are listed under 'next'")
+                "the B200 hot path covers the Laplace operator (SURVEY.md section 8); "
+                "mass equations are out of scope")
+        if spec.components == 3 and (slab_z0 or (global_cells_z and global_cells_z != mesh.cells_per_dim[2])):
+            raise NotImplementedError("z-slabs of a 3-component operator are not supported")
         if precision not in ("fp64", "fp32"):
             raise ValueError("precision must be 'fp64' or 'fp32'")
         self.spec = spec
@@ -150,6 +153,7 @@ class MatrixFreeOperator:
         d.precision = 0 if precision == "fp64" else 1
         d.brick = (C.c_int32 * 3)(*brick)
         # z-slab of a larger mesh (slabs.py): `mesh` is the slab, its extents those of the whole mesh
+        d.components = spec.components
         d.slab_z0 = int(slab_z0)
         d.global_cells_z = int(global_cells_z) if global_cells_z else mesh.cells_per_dim[2]
         self.slab_z0, self.global_cells_z = d.slab_z0, d.global_cells_z
@@ -208,8 +212,9 @@ class MatrixFreeOperator:
         raise ValueError("the operator holds no stored geometry table")
 
     def device_permutation(self) -> np.ndarray:
-        """perm[user index] = index in the library's brick numbering."""
-        perm = np.empty(self.n_dofs, dtype=np.int32)
+        """perm[node] = index in the library's brick numbering (component c of
+        that node lives at ``c * stride + perm[node]`` on the device)."""
+        perm = np.empty(self.n_dofs // self.components, dtype=np.int32)
         _lib.check(self._lib.mfcg_op_device_permutation(self._handle, _ptr(perm, C.c_int32)))
         return perm
 
@@ -268,7 +273,7 @@ class MatrixFreeOperator:
     def compute_diagonal(self) -> DiagonalPreconditioner:
         """1/diag of the GL-collocation operator, constrained entries 1
         (operator.py:380-418); ValueError when not positive definite."""
-        out = np.empty(self.n_dofs)
+        out = np.empty(self.n_dofs // self.components)
         _lib.check(self._lib.mfcg_op_diagonal(self._handle, out.ctypes.data, 0))
         return DiagonalPreconditioner(out, self)
 

@@ -31,14 +31,20 @@ NUMBERING_CASES = [
 
 CURVED_CASES = [((3, 3, 3), 3, 4, 0.1), ((4, 3, 5), 5, 6, 0.1), ((2, 2, 2), 2, 4, 0.05)]
 
+# 3-component Laplace (BP4 type): cells, p, nq, numbering, deformation, geometry variant
+VECTOR_CASES = [((3, 2, 2), 2, 3, "default", 0.0, "affine"),
+                ((4, 4, 4), 5, 6, "optimized", 0.0, "affine"),
+                ((3, 3, 3), 3, 4, "default", 0.1, "final_tensor_load"),
+                ((5, 4, 3), 4, 5, "default", 0.0, "affine")]
+
 
 def host_tables(cells, p, *, constrain=True, numbering="default", traversal="morton", batch=None,
-                deform=0.0):
+                deform=0.0, components=1):
     m = pmesh.build_cartesian_mesh(cells)
     if deform:
         m = pmesh.deform_mesh(m, deform)
-    h = dofs.distribute_dofs(m, p, 1, constrain_boundary=constrain)
-    plan = dofs.make_batches(m, batch or dofs.batch_size(p, 1, 8), traversal)
+    h = dofs.distribute_dofs(m, p, components, constrain_boundary=constrain)
+    plan = dofs.make_batches(m, batch or dofs.batch_size(p, components, 8), traversal)
     if numbering == "optimized":
         h = dofs.renumber_optimized(h, plan)
     return m, h, plan
@@ -46,13 +52,14 @@ def host_tables(cells, p, *, constrain=True, numbering="default", traversal="mor
 
 def oracle_problem(m, h, p, nq, geometry="affine", quadrature="gauss"):
     return orc.Problem(tuple(m.cells_per_dim), tuple(m.extents), m.deformation, p, nq,
-                       h.cell_index_blocks, h.constrained_dofs, h.n_dofs, geometry, quadrature)
+                       h.cell_index_blocks, h.constrained_dofs, h.n_dofs, geometry, quadrature,
+                       h.components)
 
 
 def gpu_operator(m, h, plan, p, nq, variant="affine", precision="fp64", brick=(0, 0, 0),
                  quadrature="gauss"):
     from paper_2205_08909_b200.operator import MatrixFreeOperator, OperatorSpec
-    spec = OperatorSpec("laplace", 1, p, nq, pmesh.GeometryVariant(variant), quadrature)
+    spec = OperatorSpec("laplace", h.components, p, nq, pmesh.GeometryVariant(variant), quadrature)
     return MatrixFreeOperator(spec, m, h, plan, precision=precision, brick=brick)
 
 

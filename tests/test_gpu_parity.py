@@ -270,6 +270,75 @@ def test_curved_midsize_vs_oracle_and_errors():
 
 
 # ---------------------------------------------------------------------------
+# 3 components (SURVEY.md 8f row 3, BP4 type): the scalar operator on every component
+
+from _problems import VECTOR_CASES  # noqa: E402
+
+
+@pytest.mark.parametrize("ci", range(len(VECTOR_CASES)))
+def test_three_components_vs_reference(golden, ci):
+    S = _solvers()
+    cells, p, nq, numbering, amp, variant = VECTOR_CASES[ci]
+    g = golden["vector3"]
+    m, h, plan = host_tables(cells, p, numbering=numbering, deform=amp, components=3)
+    op = gpu_operator(m, h, plan, p, nq, variant=variant)
+    assert op.components == 3 and op.n_dofs == h.n_dofs == op.info()["n_dofs"]
+    u = g[f"v{ci}_u"]
+    Au = op.apply(u)
+    assert rel(Au, g[f"v{ci}_Au"]) < 1e-12
+    assert np.array_equal(Au[h.constrained_dofs], u[h.constrained_dofs])      # operator.py:359-360
+    minv = op.compute_diagonal()
+    assert minv.inverse_diagonal.shape == (h.n_dofs // 3,)                    # operator.py:90
+    assert rel(minv.inverse_diagonal, g[f"v{ci}_invdiag"]) < 1e-12
+    b = g[f"v{ci}_b"]
+    for name in ("pcg", "combined_pcg", "combined_cg"):
+        R = g[f"v{ci}_{name}_hist"]
+        for mv in ((minv, minv.inverse_diagonal.copy()) if name != "combined_cg" else (None,)):
+            # the operator's own diagonal (device copy / on-the-fly) and a caller-supplied array
+            res = S.solve(name, op, b, minv=mv, config=S.SolverConfig(fixed_iterations=30))
+            H = hist_array(res.history)
+            assert res.iterations == 30 and res.matvecs == 30
+            # strict while the residual is far from the rounding floor of these tiny systems
+            # (CG amplifies summation-order noise once it is not)
+            k = np.flatnonzero(R[:20, 3] > 1e-6)
+            assert len(k) >= 8
+            assert (np.abs(H[k, 3] - R[k, 3]) / R[k, 3]).max() < 1e-10, name
+            assert rel(H[k, :2], R[k, :2]) < 1e-10, name
+            assert rel(res.x, g[f"v{ci}_{name}_x"]) < 1e-8, name
+    unf = S.solve("combined_pcg", op, b, minv=minv, config=S.SolverConfig(fixed_iterations=30, fused=False))
+    R = g[f"v{ci}_combined_pcg_hist"]
+    k = np.flatnonzero(R[:20, 3] > 1e-6)
+    assert rel(hist_array(unf.history)[k, 3], R[k, 3]) < 1e-10
+    with pytest.raises(ValueError):            # one diagonal value per NODE (solvers.py:617-619)
+        S.solve("combined_pcg", op, b, minv=np.ones(h.n_dofs))
+
+
+def test_three_components_midsize_vs_oracle():
+    """Q5, ragged brick grid, three components against the CPU oracle; a vector whose components
+    differ must not mix them."""
+    cells, p, nq = (9, 6, 7), 5, 6
+    m, h, plan = host_tables(cells, p, components=3)
+    prob = oracle_problem(m, h, p, nq)
+    op = gpu_operator(m, h, plan, p, nq)
+    u = np.random.default_rng(12).standard_normal(h.n_dofs)
+    assert rel(op.apply(u), orc.apply(prob, u)) < 1e-12
+    only1 = np.zeros_like(u)
+    only1[1::3] = u[1::3]
+    out = op.apply(only1)
+    free = np.ones(h.n_dofs, bool)
+    free[h.constrained_dofs] = False
+    assert not out[0::3][free[0::3]].any() and not out[2::3][free[2::3]].any()
+    with pytest.raises(ValueError):            # partial-node constraints (dofs.py:329-330)
+        bad = dofs_replace_constraints(h, h.constrained_dofs[1:])
+        gpu_operator(m, bad, plan, p, nq)
+
+
+def dofs_replace_constraints(h, constrained):
+    import dataclasses
+    return dataclasses.replace(h, constrained_dofs=np.asarray(constrained, dtype=np.int64))
+
+
+# ---------------------------------------------------------------------------
 # BASELINE sizes: no oracle can run there, so size-independent properties (the prompt's
 # "encode -> decode round trips, linearity, checksums"): true vs recurred residual, merged vs
 # standard scalars, linearity of the operator, constrained rows copied through bit-exactly.

@@ -18,7 +18,8 @@ def test_table_and_errors():
     with pytest.raises(ValueError):
         harness.assemble_problem("BP9", 2, (2, 2, 2))
     with pytest.raises(NotImplementedError):
-        harness.assemble_problem("BP4", 2, (2, 2, 2))
+        harness.assemble_problem("BP2", 2, (2, 2, 2))      # mass operators are out of scope
+    assert harness.BENCHMARK_PROBLEMS["BP4"].operator_spec(3).components == 3
     u = harness.manufactured_solution(np.array([[0.5, 0.5, 0.5], [0.0, 0.3, 0.7]]))
     assert u[0] == pytest.approx(1.0) and abs(u[1]) < 1e-15
     assert harness.manufactured_forcing(np.array([[0.5, 0.5, 0.5]]), "laplace")[0] == pytest.approx(3 * math.pi ** 2)
@@ -42,6 +43,15 @@ def test_bp5_energy_and_record():
     op3, b3, minv3 = harness.assemble_problem("BP3", 3, (5, 5, 5), geometry=GeometryVariant.AFFINE, deform=0.0)
     r3 = solve("combined_pcg", op3, b3, minv=minv3, config=SolverConfig(tolerance=1e-10, max_iterations=2000))
     assert r3.x @ b3 == pytest.approx(3.0 * math.pi ** 2 / 8.0, rel=1e-3)
+    # BP4: three components, each carrying the same manufactured problem -> three times the energy
+    op4, b4, minv4 = harness.assemble_problem("BP4", 3, (5, 5, 5), geometry=GeometryVariant.AFFINE, deform=0.0)
+    assert op4.n_dofs == 3 * 16 ** 3 and np.array_equal(b4[0::3], b3) and np.array_equal(b4[2::3], b3)
+    r4 = solve("combined_pcg", op4, b4, minv=minv4, config=SolverConfig(tolerance=1e-10, max_iterations=2000))
+    assert r4.converged and r4.x @ b4 == pytest.approx(9.0 * math.pi ** 2 / 8.0, rel=1e-3)
+    assert np.max(np.abs(r4.x[1::3] - r3.x)) < 1e-8
+    rec4 = harness.run_benchmark("BP4", 3, (5, 5, 5), "combined_pcg", iterations=10, repeats=1,
+                                 geometry=GeometryVariant.AFFINE, deform=0.0)
+    assert rec4.n_dofs == 3 * 16 ** 3 and rec4.iterations == 10
 
 
 def test_manufactured_rhs_matches_reference(golden):
@@ -61,3 +71,11 @@ def test_manufactured_rhs_matches_reference(golden):
     b = harness.build_rhs(f)
     ref = golden["harness"]["bp5_p3_322_rhs"]
     assert np.max(np.abs(b - ref)) / np.max(np.abs(ref)) < 1e-13
+    # BP4: p + 2 Gauss points, three interleaved components (reference bench.py:113-116)
+    f.spec = harness.BENCHMARK_PROBLEMS["BP4"].operator_spec(3)
+    f.handler = dofs.distribute_dofs(m, 3, 3, True)
+    f.quadrature = tensor.gauss_quadrature(5)
+    f.basis = tensor.lagrange_basis(3, f.quadrature)
+    b4 = harness.build_rhs(f)
+    ref4 = golden["harness"]["bp4_p3_322_rhs"]
+    assert b4.shape == ref4.shape and np.max(np.abs(b4 - ref4)) / np.max(np.abs(ref4)) < 1e-13

@@ -143,3 +143,16 @@ def test_mesh_layout_and_text_roundtrip():
     assert np.allclose(d.map_points(face), face)
     back = pmesh.mesh_from_text(pmesh.mesh_to_text(d))
     assert back.cells_per_dim == d.cells_per_dim and back.deformation == d.deformation
+
+
+def test_three_component_numbering_matches_reference(golden):
+    """distribute_dofs / renumber_optimized with components = 3 (reference dofs.py:138-179, 304-388)."""
+    from _problems import VECTOR_CASES
+    g = golden["vector3"]
+    for ci, (cells, p, nq, numbering, amp, variant) in enumerate(VECTOR_CASES):
+        m, h, plan = host_tables(cells, p, numbering=numbering, deform=amp, components=3)
+        assert h.components == 3 and h.n_dofs == 3 * int(np.prod([c * p + 1 for c in cells]))
+        assert np.array_equal(h.cell_index_blocks, g[f"v{ci}_blocks"])
+        assert np.array_equal(h.constrained_dofs, g[f"v{ci}_constrained"])
+        if numbering == "optimized":
+            assert np.array_equal(h.permutation, g[f"v{ci}_permutation"])

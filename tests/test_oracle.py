@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 import mfcg_oracle as orc
-from _problems import APPLY_CASES, CURVED_CASES, hist_array, host_tables, oracle_problem, rel
+from _problems import APPLY_CASES, CURVED_CASES, VECTOR_CASES, hist_array, host_tables, oracle_problem, rel
 
 
 def test_quadrature_closed_forms():
@@ -148,6 +148,32 @@ def test_curved_geometry_matches_reference(golden, ci):
     assert rel(sym, ft) < 1e-12
     assert rel(orc.apply(prob, g[f"k{ci}_u"]), g[f"k{ci}_Au"]) < 1e-12
     assert rel(orc.inverse_diagonal(prob), g[f"k{ci}_invdiag"]) < 1e-12
+
+
+@pytest.mark.parametrize("ci", range(len(VECTOR_CASES)))
+def test_three_component_operator_and_solvers_match_reference(golden, ci):
+    """BP4-type vector Laplacian: the scalar operator on each interleaved component, one
+    diagonal value per node replicated (reference operator.py:92-99, 256-281; solvers.py:612-621)."""
+    cells, p, nq, numbering, amp, variant = VECTOR_CASES[ci]
+    g = golden["vector3"]
+    m, h, plan = host_tables(cells, p, numbering=numbering, deform=amp, components=3)
+    prob = oracle_problem(m, h, p, nq, geometry="affine" if variant == "affine" else "curved")
+    assert prob.n_nodes * 3 == h.n_dofs
+    assert rel(orc.apply(prob, g[f"v{ci}_u"]), g[f"v{ci}_Au"]) < 1e-12
+    inv = orc.inverse_diagonal(prob)
+    assert inv.shape == (prob.n_nodes,)
+    assert rel(inv, g[f"v{ci}_invdiag"]) < 1e-12
+    b = g[f"v{ci}_b"]
+    full = np.repeat(inv, 3)
+    x, k, res, conv, hist = orc.pcg(lambda v: orc.apply(prob, v), b, full, fixed_iterations=30)
+    R = g[f"v{ci}_pcg_hist"]
+    assert rel(hist_array(hist)[:20], R[:20]) < 1e-9
+    x, k, res, conv, hist = orc.combined_pcg(lambda v: orc.apply(prob, v), b, full, fixed_iterations=30)
+    R = g[f"v{ci}_combined_pcg_hist"]
+    assert rel(hist_array(hist)[:20], R[:20]) < 1e-9
+    assert rel(x, g[f"v{ci}_combined_pcg_x"]) < 1e-7
+    x, k, res, conv, hist = orc.combined_pcg(lambda v: orc.apply(prob, v), b, None, fixed_iterations=30)
+    assert rel(hist_array(hist)[:20], g[f"v{ci}_combined_cg_hist"][:20]) < 1e-9
 
 
 def test_c_oracle_matches_numpy_oracle_and_reference(golden):

@@ -9,6 +9,5 @@ lscpu | head -20 > gpurun_out/lscpu_box.txt
 CMD="python bench.py --cells 73 73 73 --iters 8 --steps 1 --warmup 3 --no-cpu-baseline"
 $CMD > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu1.log 2>&1
-$CMD > gpurun_out/plain2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_brick -s 6 -c 2 -o gpurun_out/prof_brick -f $CMD > gpurun_out/ncu2.log 2>&1
-tail -1 gpurun_out/ncu2.log
+# the full capture of the brick kernel is a separate call: tools/gpu_prof.sh ncu
+python bench.py --cells 73 73 73 --components 3 --steps 2 --no-cpu-baseline > gpurun_out/bench_bp4type_73.json 2> gpurun_out/bench_bp4.err; tail -2 gpurun_out/bench_bp4.err

@@ -43,7 +43,7 @@ tr = [val(r, 'dram__bytes_read.sum') + val(r, 'dram__bytes_write.sum') for r in 
 json.dump({"k_brick_merged_bytes_per_launch": sum(tr) / len(tr), "launches": tr,
            "workload": "73^3 cells Q5 (49027896 DoFs)", "bytes_per_dof": sum(tr) / len(tr) / 49027896,
            "source": "ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum, two consecutive launches "
-                     "(one with, one without the x update); model 72 / 56 B per DoF on interior DoFs"},
+                     "(one with, one without the x update); model 64 / 48 B per DoF on interior DoFs (the separable 1/diag is computed, not loaded)"},
           open('profiles/traffic.json', 'w'), indent=1)
 print("traffic B/DoF", [t / 49027896 for t in tr])
 subprocess.run([sys.executable, "tools/ncu_summary.py", "gpurun_out/prof_brick.ncu-rep", f"profiles/{tag}_ncu_brick.txt",
