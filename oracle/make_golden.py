@@ -239,6 +239,22 @@ def vector3():
     np.savez_compressed(OUT / "vector3.npz", **out)
 
 
+def locality():
+    """Liveliness reports of the reference (locality.py:216-227) for config 1 and a Q5 mesh."""
+    from mfcg.locality import liveliness
+    out = {}
+    for ci, (cells, p) in enumerate([((8, 8, 8), 4), ((6, 5, 4), 5)]):
+        for numbering in ("default", "optimized"):
+            op, h, plan, mesh = build(cells, p, p + 1, numbering=numbering)
+            rep = liveliness(compute_range_schedule(h, plan))
+            key = f"l{ci}_{numbering}"
+            out[key + "_distances"] = rep.distances
+            out[key + "_cdf_distances"] = rep.cdf_distances
+            out[key + "_cdf_fractions"] = rep.cdf_fractions
+            out[key + "_scalars"] = np.array([rep.n_batches, rep.same_batch_fraction, rep.n_ranges])
+    np.savez_compressed(OUT / "locality.npz", **out)
+
+
 if __name__ == "__main__":
     tables()
     harness_rhs()
@@ -248,5 +264,6 @@ if __name__ == "__main__":
     q5_small()
     curved()
     vector3()
+    locality()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)
