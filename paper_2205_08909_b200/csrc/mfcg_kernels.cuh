@@ -180,7 +180,11 @@ template <int P, int G = 0> struct Geo {
   template <typename T> __host__ __device__ static constexpr size_t red_offset() {
     return (256 + sizeof(T) * (size_t)(NRING * RB * PLANE + PLANE + NTILE * NCELL * TILE) + 15) & ~(size_t)15;
   }
-  template <typename T> __host__ __device__ static constexpr size_t smem_bytes() { return red_offset<T>() + 8 * 7 * 32; }
+  // separable path: table of the P^3 distinct 1/diag values of brick-interior DoFs (affine meshes)
+  template <typename T> __host__ __device__ static constexpr size_t dtab_offset() { return red_offset<T>() + 8 * 7 * 32; }
+  template <typename T> __host__ __device__ static constexpr size_t smem_bytes() {
+    return dtab_offset<T>() + (G == 0 ? ((sizeof(T) * (size_t)(P * P * P) + 15) & ~(size_t)15) : 0);
+  }
 };
 
 // 1D matrices of the separable (Cartesian/affine) cell operator
@@ -490,6 +494,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
   T* Bs = A + NCELL * TILE;
   constexpr size_t RED_OFF = Geo<P, G>::template red_offset<T>();
   double* red = reinterpret_cast<double*>(smem_raw + RED_OFF);
+  T* dtab = reinterpret_cast<T*>(smem_raw + Geo<P, G>::template dtab_offset<T>());
 
 #ifdef MFCG_TIMING
   __shared__ unsigned long long tcnt[16];
@@ -520,6 +525,9 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
     mbar_init(&bars[3], NT_C);
   }
   for (int i = tid; i < PLANE; i += NT_C + NT_P) carry[i] = (T)0;
+  if (MODE == 1 && G == 0 && tab.diag_onfly)
+    for (int i = tid; i < P * P * P; i += NT_C + NT_P)
+      dtab[i] = diag_inverse_onfly<T, N>(tab, i % P, (i / P) % P, i / (P * P));
   __syncthreads();
 
   const int fw = Lx + 1, fp = fw * (Ly + 1);
@@ -609,7 +617,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             T rnew = (T)0;
             if (MODE == 1) {
               const i64 gi = gbase + it;
-              if (tab.diag_onfly) mm[c] = diag_inverse_onfly<T, N>(tab, (im + 1) % P, (jm + 1) % P, (Kfirst + kk) % P);
+              if (G == 0 && tab.diag_onfly) mm[c] = dtab[(((Kfirst + kk) % P) * P + (jm + 1) % P) * P + (im + 1) % P];
               T r = rr[c], p = pp[c];
               if (xmode) {
                 T x = xx[c];
@@ -701,12 +709,12 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
               const i64 gi = gbase + it;
               MFCG_CHECK(gi >= 0 && gi < n_int);
               rr[c] = R[gi]; vv[c] = V[gi]; pp[c] = Pv[gi];
-              if (tab.diag_onfly) {
+              if (G == 0 && tab.diag_onfly) {
                 const int kk = (int)__umulhi((unsigned)it, n2d_magic);
                 const int rem2 = it - kk * nint2d;
                 const int jm = (int)(((unsigned)rem2 * lxm_magic) >> 16);
                 const int im = rem2 - jm * lxm;
-                mm[c] = diag_inverse_onfly<T, N>(tab, (im + 1) % P, (jm + 1) % P, (Klo + kk) % P);
+                mm[c] = dtab[(((Klo + kk) % P) * P + (jm + 1) % P) * P + (im + 1) % P];
               } else {
                 mm[c] = Minv[gi];
               }

@@ -45,6 +45,6 @@ def test_brick_schedule_properties():
     assert rep.same_batch_fraction > 0.8 * info["n_interior"] / h.n_dofs
     assert sum(len(a) for a in sch.pre_schedule) == sch.n_ranges == sum(len(a) for a in sch.post_schedule)
     # one brick: everything is produced and finished in it
-    m1, h1, plan1 = host_tables((3, 3, 2), 3)
-    rep1 = locality.liveliness(locality.brick_schedule(gpu_operator(m1, h1, plan1, 3, 4)))
+    m1, h1, plan1 = host_tables((2, 2, 2), 3)
+    rep1 = locality.liveliness(locality.brick_schedule(gpu_operator(m1, h1, plan1, 3, 4, brick=(2, 2, 2))))
     assert rep1.n_batches == 1 and rep1.same_batch_fraction == 1.0
