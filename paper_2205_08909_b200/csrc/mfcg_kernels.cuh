@@ -165,14 +165,26 @@ inline bool brick_caps(int p, int gclass, int* bx, int* by) {
 
 template <int P, int G = 0> struct Geo {
   static constexpr int N = P + 1;
-  // tile strides: element (k, j, i) of a cell tile sits at k*PSTR + j*RS + i; odd row stride.
-  // (Dense rows with planes padded to 38 doubles plus permuted line orders make the y and z
-  // sweeps bank-conflict free for N = 6, but measured 7 % slower: profiles/r01_notes.md.)
-  static constexpr int RS = (N % 2 == 0) ? N + 1 : N;
-  static constexpr int PSTR = N * RS;
-  static constexpr int TILE = N * PSTR;
-  static constexpr int NTILE = G ? 3 : 2;               // scratch tiles per cell
   static constexpr int NCELL = Cfg<P, G>::BX * Cfg<P, G>::BY;
+  // Math thread -> (cell, line slot) mapping.  CELL_MINOR: consecutive threads work on the SAME
+  // line of consecutive cells, so the 16 lanes of a half-warp (the unit of a 64-bit shared-memory
+  // access) touch one tile offset in 16 different tiles; with an odd tile stride those are 16
+  // different banks in every sweep, whatever the line.  Needs a multiple of 16 cells per layer.
+  static constexpr bool CELL_MINOR = (G == 0) && (NCELL % 16 == 0);
+  // tile strides: element (k, j, i) of a cell tile sits at k*PSTR + j*RS + i.
+  //  - CELL_MINOR: dense rows; tile stride odd and = P mod 16 (then the gather, whose lanes walk
+  //    along x through consecutive cells, is conflict free as well)
+  //  - otherwise: odd row stride (2-way conflicts in the y and z sweeps)
+  static constexpr int RS = CELL_MINOR ? N : ((N % 2 == 0) ? N + 1 : N);
+  static constexpr int PSTR = N * RS;
+  static constexpr int tile_stride() {
+    if (!CELL_MINOR) return N * PSTR;
+    int t = N * PSTR;
+    while (t % 2 == 0 || t % 16 != P % 16) ++t;
+    return t;
+  }
+  static constexpr int TILE = tile_stride();
+  static constexpr int NTILE = G ? 3 : 2;               // scratch tiles per cell
   static constexpr int WX = (P * Cfg<P, G>::BX + 1) | 1; // window row stride, odd
   static constexpr int PLANE = WX * (P * Cfg<P, G>::BY + 1);
   static constexpr int RB = 2 * P + 1;                  // lattice planes in the ring: two layers share one
@@ -740,7 +752,8 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
     // Fixed ownership: TPC threads per cell, thread q of a cell owns lines q, q+TPC, ... of
     // that cell in every sweep of every layer, so all index arithmetic is hoisted.
     constexpr int TPC = Cfg<P, G>::TPC, LPT = (N * N + TPC - 1) / TPC;
-    const int cell = tid / TPC, q = tid - cell * TPC;
+    constexpr bool CM = Geo<P, G>::CELL_MINOR;
+    const int cell = CM ? tid % NCELL : tid / TPC, q = CM ? tid / NCELL : tid - cell * TPC;
     const bool has_cell = cell < bcx * bcy;
     const int cy = has_cell ? cell / bcx : 0, cx = has_cell ? cell - cy * bcx : 0;
     T* const At = A + cell * TILE;
