@@ -140,8 +140,13 @@ class Engine : public EngineBase {
         for (int j = i; j < H; ++j) Ao[sym_idx(i, j)] = (T)(0.5 * (A[i * N + j] - A[i * N + (N - 1 - j)]));
     };
     pack(M, tab_.Me, tab_.Mo);
-    pack(K, tab_.Ke, tab_.Ko);
-    for (int d = 0; d < 3; ++d) tab_.g[d] = (T)(det / (c_->h[d] * c_->h[d]));
+    for (int d = 0; d < 3; ++d) {
+      const double gd = det / (c_->h[d] * c_->h[d]);
+      tab_.g[d] = (T)gd;
+      std::vector<double> Kd(K);
+      for (double& v : Kd) v *= gd;
+      pack(Kd, tab_.Ke[d], tab_.Ko[d]);
+    }
     // separable factors of the GL-collocation diagonal (index 0: sum over the two cells at a cell boundary)
     for (int i = 0; i < P; ++i) {
       double dd0 = 0.0, ddp = 0.0, ddi = 0.0;

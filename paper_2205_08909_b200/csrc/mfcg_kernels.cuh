@@ -214,7 +214,8 @@ template <int N> struct EOShape {
   static constexpr int NE = HE * (HE + 1) / 2, NO = H * (H + 1) / 2 > 0 ? H * (H + 1) / 2 : 1;
 };
 template <typename T, int N> struct SepTables {
-  T Me[EOShape<N>::NE], Mo[EOShape<N>::NO], Ke[EOShape<N>::NE], Ko[EOShape<N>::NO];
+  // K is stored once per direction, pre-scaled by g_d (saves the per-line scaling multiplies)
+  T Me[EOShape<N>::NE], Mo[EOShape<N>::NO], Ke[3][EOShape<N>::NE], Ko[3][EOShape<N>::NO];
   T g[3];
   // Jacobi diagonal of the GL-collocation operator on an affine mesh, separable per direction
   // (operator.py:380-418): diag(I,J,K) = gx da[i] wa[j] wa[k] + gy wa[i] da[j] wa[k] + gz wa[i] wa[j] da[k]
@@ -435,22 +436,29 @@ __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned coun
 __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifndef MFCG_WAIT_HINT
+#define MFCG_WAIT_HINT 20000
+#endif
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
   unsigned ok;
+#ifdef MFCG_WAIT_SLEEP
+  for (;;) {  // explicit back-off between polls
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(ok)
+                 : "r"(smem_u32(bar)), "r"(parity)
+                 : "memory");
+    if (ok) break;
+    __nanosleep(MFCG_WAIT_SLEEP);
+  }
+#else
   do {  // the hint lets the hardware park the warp until the phase flips instead of spinning
     asm volatile(
-#ifdef MFCG_WAIT_NOHINT
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-#else
         "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity), "r"(20000u)
+        : "r"(smem_u32(bar)), "r"(parity), "r"((unsigned)MFCG_WAIT_HINT)
         : "memory");
-#endif
   } while (!ok);
+#endif
 }
 // L2 prefetch of a contiguous run (TMA-class bulk prefetch, no registers or shared memory):
 // [ptr + first, ptr + first + count) elements, widened to 16-byte alignment inside [0, limit)
@@ -467,6 +475,18 @@ __device__ __forceinline__ void prefetch_l2_run(const T* ptr, i64 first, i64 cou
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr + lo), "r"(bytes) : "memory");
 }
 
+// Hand-over between memory and math warps through hardware named barriers (ids 2..5) instead of
+// mbarrier polling: the arriving role does not block, the waiting role sleeps in the barrier unit.
+template <int COUNT> __device__ __forceinline__ void named_arrive(int id) {
+  __threadfence_block();
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "n"(COUNT) : "memory");
+}
+template <int COUNT> __device__ __forceinline__ void named_wait(int id) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(COUNT) : "memory");
+}
+#ifndef MFCG_NAMED_BAR
+#define MFCG_NAMED_BAR 0
+#endif
 template <int COUNT> __device__ __forceinline__ void math_barrier() {
   asm volatile("bar.sync 1, %0;" ::"n"(COUNT) : "memory");
 }
@@ -573,14 +593,16 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
         if (ptid == 0) prefetch_l2_run(Pv, first, count, g.n_dofs);
         if (ptid == 1) prefetch_l2_run(R, first, count, g.n_dofs);
         if (ptid == 2) prefetch_l2_run(V, first, count, g.n_dofs);
-        if (ptid == 3) prefetch_l2_run(Minv, first, count, g.n_dofs);
+        if (ptid == 3 && !(G == 0 && tab.diag_onfly)) prefetch_l2_run(Minv, first, count, g.n_dofs);
         if (ptid == 4 && xmode) prefetch_l2_run(X, first, count, g.n_dofs);
       }
     };
-    // L2 prefetch distance in layers.  Measured (profiles/r01_notes.md): no gain in time and
-    // +0.9 GB of DRAM reads per launch at 73^3 (lines fetched twice), so it is off by default.
+    // L2 prefetch distance in layers (TMA-class bulk prefetch of the next layer's interior runs).
+    // Measured (profiles/r01_notes.md): one layer ahead shortens the kernel by 6 % once the sweeps
+    // are bank-conflict free (the memory warps then wait on load latency), DRAM traffic +2 %;
+    // two layers ahead is worse than one.
 #ifndef MFCG_L2_PREFETCH
-#define MFCG_L2_PREFETCH 0
+#define MFCG_L2_PREFETCH 1
 #endif
     constexpr int PF = MFCG_L2_PREFETCH;
     for (int Lq = 0; Lq < PF; ++Lq) prefetch_layer(Lq);
@@ -588,7 +610,10 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
     for (int L = 0; L < bcz + 2; ++L) {
       const int stage = L & 1;
       if (PF > 0) prefetch_layer(L + PF);
-      if (L >= 2) mbar_wait(&bars[2 + stage], ((L >> 1) - 1) & 1);  // layer L-2 consumed
+      if (L >= 2) {  // layer L-2 consumed
+        if (MFCG_NAMED_BAR) named_wait<NT_C + NT_P>(4 + stage);
+        else mbar_wait(&bars[2 + stage], ((L >> 1) - 1) & 1);
+      }
       MFCG_TOC(tp, 0);
       if (L < bcz) {
         // ---- fill the ring with the planes layer L adds (plane 0 is shared with layer L-1)
@@ -700,7 +725,8 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             ring[slot + (jm + 1) * WX + im + 1] = mk ? (T)0 : pv;
           }
         }
-        mbar_arrive(&bars[stage]);  // layer L full
+        if (MFCG_NAMED_BAR) named_arrive<NT_C + NT_P>(2 + stage);  // layer L full
+        else mbar_arrive(&bars[stage]);
         MFCG_TOC(tp, 1);
       }
       if (MODE == 1 && !ONCHIP && L >= 2 && !(MFCG_SKIP & 4)) {
@@ -766,7 +792,8 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
       const int stage = L & 1;
       const int s0 = (L * P) % RB;
       if (L > 0) math_barrier<NT_C>();        // every math thread is done with the previous gather's tiles
-      mbar_wait(&bars[stage], (L >> 1) & 1);  // layer L full
+      if (MFCG_NAMED_BAR) named_wait<NT_C + NT_P>(2 + stage);  // layer L full
+      else mbar_wait(&bars[stage], (L >> 1) & 1);
       MFCG_TOC(tc, 4);
 
       if (G >= 1) {
@@ -961,9 +988,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             for (int i = 0; i < N; ++i) ao[i] = out[i];
   #pragma unroll
             for (int i = 0; i < HE; ++i) { se[i] = 0; so[i] = 0; }
-            eo_mul<N>(tab.Ke, tab.Ko, e, o, se, so);
-  #pragma unroll
-            for (int i = 0; i < HE; ++i) { se[i] *= tab.g[0]; so[i] *= tab.g[0]; }
+            eo_mul<N>(tab.Ke[0], tab.Ko[0], e, o, se, so);
             eo_join<N>(se, so, out);
   #pragma unroll
             for (int i = 0; i < N; ++i) bo[i] = out[i];
@@ -992,9 +1017,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             T se[HE], so[HE], out[N];
   #pragma unroll
             for (int i2 = 0; i2 < HE; ++i2) { se[i2] = 0; so[i2] = 0; }
-            eo_mul<N>(tab.Ke, tab.Ko, ea, oa, se, so);  // K a
-  #pragma unroll
-            for (int i2 = 0; i2 < HE; ++i2) { se[i2] *= tab.g[1]; so[i2] *= tab.g[1]; }
+            eo_mul<N>(tab.Ke[1], tab.Ko[1], ea, oa, se, so);  // gy K a
             eo_mul<N>(tab.Me, tab.Mo, eb, ob, se, so);  // + M b
             eo_join<N>(se, so, out);
   #pragma unroll
@@ -1030,9 +1053,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             T se[HE], so[HE], out[N];
   #pragma unroll
             for (int i2 = 0; i2 < HE; ++i2) { se[i2] = 0; so[i2] = 0; }
-            eo_mul<N>(tab.Ke, tab.Ko, ec, oc, se, so);  // K c
-  #pragma unroll
-            for (int i2 = 0; i2 < HE; ++i2) { se[i2] *= tab.g[2]; so[i2] *= tab.g[2]; }
+            eo_mul<N>(tab.Ke[2], tab.Ko[2], ec, oc, se, so);  // gz K c
             eo_mul<N>(tab.Me, tab.Mo, ed, od, se, so);  // + M de
             eo_join<N>(se, so, out);
   #pragma unroll
@@ -1108,7 +1129,9 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
 #pragma unroll
           for (int qq = 0; qq < 7; ++qq) red[(tid >> 5) * 7 + qq] += s[qq];
       }
-      mbar_arrive(&bars[2 + stage]);  // layer L consumed (orders the v stores before the post loads)
+      // layer L consumed (orders the v stores before the post loads)
+      if (MFCG_NAMED_BAR) named_arrive<NT_C + NT_P>(4 + stage);
+      else mbar_arrive(&bars[2 + stage]);
       MFCG_TOC(tc, 9);
     }
   }
