@@ -189,8 +189,9 @@ template <int P, int G = 0> struct Geo {
   static constexpr int PLANE = WX * (P * Cfg<P, G>::BY + 1);
   static constexpr int RB = 2 * P + 1;                  // lattice planes in the ring: two layers share one
   static constexpr int NRING = Cfg<P, G>::ONCHIP ? 3 : 1;  // p' (+ r', 1/diag)
+  static constexpr int HEADER = 320;                    // 27 entity starts, 6 mbarriers
   template <typename T> __host__ __device__ static constexpr size_t red_offset() {
-    return (256 + sizeof(T) * (size_t)(NRING * RB * PLANE + PLANE + NTILE * NCELL * TILE) + 15) & ~(size_t)15;
+    return (HEADER + sizeof(T) * (size_t)(NRING * RB * PLANE + PLANE + NTILE * NCELL * TILE) + 15) & ~(size_t)15;
   }
   // separable path: table of the P^3 distinct 1/diag values of brick-interior DoFs (affine meshes)
   template <typename T> __host__ __device__ static constexpr size_t dtab_offset() { return red_offset<T>() + 8 * 7 * 32; }
@@ -475,18 +476,6 @@ __device__ __forceinline__ void prefetch_l2_run(const T* ptr, i64 first, i64 cou
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr + lo), "r"(bytes) : "memory");
 }
 
-// Hand-over between memory and math warps through hardware named barriers (ids 2..5) instead of
-// mbarrier polling: the arriving role does not block, the waiting role sleeps in the barrier unit.
-template <int COUNT> __device__ __forceinline__ void named_arrive(int id) {
-  __threadfence_block();
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "n"(COUNT) : "memory");
-}
-template <int COUNT> __device__ __forceinline__ void named_wait(int id) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(COUNT) : "memory");
-}
-#ifndef MFCG_NAMED_BAR
-#define MFCG_NAMED_BAR 0
-#endif
 template <int COUNT> __device__ __forceinline__ void math_barrier() {
   asm volatile("bar.sync 1, %0;" ::"n"(COUNT) : "memory");
 }
@@ -516,9 +505,10 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
                 NT_C = Cfg<P, G>::NT_C, NT_P = Cfg<P, G>::NT_P, KC = Cfg<P, G>::KC, HE = EOShape<N>::HE;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   i64* st27 = reinterpret_cast<i64*>(smem_raw);                               // 27 entity starts
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem_raw + 224);  // full[2], empty[2]
+  // full[2] (memory -> math), ringfree[2] (ring planes of a layer read), vdone[2] (v of a layer stored)
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem_raw + 224);
   constexpr bool ONCHIP = Cfg<P, G>::ONCHIP && MODE == 1;
-  T* ring = reinterpret_cast<T*>(smem_raw + 256);
+  T* ring = reinterpret_cast<T*>(smem_raw + Geo<P, G>::HEADER);
   T* Rring = ring + RB * PLANE;              // only with Cfg::ONCHIP
   T* Mring = Rring + RB * PLANE;
   T* carry = ring + Geo<P, G>::NRING * RB * PLANE;
@@ -555,6 +545,8 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
     mbar_init(&bars[1], NT_P);
     mbar_init(&bars[2], NT_C);
     mbar_init(&bars[3], NT_C);
+    mbar_init(&bars[4], NT_C);
+    mbar_init(&bars[5], NT_C);
   }
   for (int i = tid; i < PLANE; i += NT_C + NT_P) carry[i] = (T)0;
   if (MODE == 1 && G == 0 && tab.diag_onfly)
@@ -610,10 +602,8 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
     for (int L = 0; L < bcz + 2; ++L) {
       const int stage = L & 1;
       if (PF > 0) prefetch_layer(L + PF);
-      if (L >= 2) {  // layer L-2 consumed
-        if (MFCG_NAMED_BAR) named_wait<NT_C + NT_P>(4 + stage);
-        else mbar_wait(&bars[2 + stage], ((L >> 1) - 1) & 1);
-      }
+      // the ring planes layer L overwrites were last read by the x sweep of layer L-2
+      if (L >= 2 && L < bcz) mbar_wait(&bars[2 + stage], ((L >> 1) - 1) & 1);
       MFCG_TOC(tp, 0);
       if (L < bcz) {
         // ---- fill the ring with the planes layer L adds (plane 0 is shared with layer L-1)
@@ -725,11 +715,11 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             ring[slot + (jm + 1) * WX + im + 1] = mk ? (T)0 : pv;
           }
         }
-        if (MFCG_NAMED_BAR) named_arrive<NT_C + NT_P>(2 + stage);  // layer L full
-        else mbar_arrive(&bars[stage]);
+        mbar_arrive(&bars[stage]);  // layer L full
         MFCG_TOC(tp, 1);
       }
       if (MODE == 1 && !ONCHIP && L >= 2 && !(MFCG_SKIP & 4)) {
+        mbar_wait(&bars[4 + stage], ((L >> 1) - 1) & 1);  // v of layer L-2 stored
         // ---- post sums of layer L-2 (solvers.py:692-698): its v is final and, like r, p and
         // 1/diag, still resident in L2; one contiguous run per vector
         const int Lp = L - 2;
@@ -792,8 +782,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
       const int stage = L & 1;
       const int s0 = (L * P) % RB;
       if (L > 0) math_barrier<NT_C>();        // every math thread is done with the previous gather's tiles
-      if (MFCG_NAMED_BAR) named_wait<NT_C + NT_P>(2 + stage);  // layer L full
-      else mbar_wait(&bars[stage], (L >> 1) & 1);
+      mbar_wait(&bars[stage], (L >> 1) & 1);  // layer L full
       MFCG_TOC(tc, 4);
 
       if (G >= 1) {
@@ -850,6 +839,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             for (int i = 0; i < N; ++i) At[k * PSTR + j * RS + i] = out[i];
           }
         }
+        if (!ONCHIP) mbar_arrive(&bars[2 + stage]);  // this thread has read its ring rows of layer L
         math_barrier<NT_C>();
         sweep(1, 0, false, false, At, 0, At);
         math_barrier<NT_C>();
@@ -994,6 +984,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             for (int i = 0; i < N; ++i) bo[i] = out[i];
           }
         }
+        if (!ONCHIP) mbar_arrive(&bars[2 + stage]);  // this thread has read its ring rows of layer L
         MFCG_TOC(tc, 5);
         math_barrier<NT_C>();
         MFCG_TOC(tc, 8);
@@ -1129,9 +1120,8 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
 #pragma unroll
           for (int qq = 0; qq < 7; ++qq) red[(tid >> 5) * 7 + qq] += s[qq];
       }
-      // layer L consumed (orders the v stores before the post loads)
-      if (MFCG_NAMED_BAR) named_arrive<NT_C + NT_P>(4 + stage);
-      else mbar_arrive(&bars[2 + stage]);
+      if (ONCHIP) mbar_arrive(&bars[2 + stage]);  // the on-chip post reads the ring in the gather
+      mbar_arrive(&bars[4 + stage]);  // v of layer L stored (orders the v stores before the post loads)
       MFCG_TOC(tc, 9);
     }
   }
