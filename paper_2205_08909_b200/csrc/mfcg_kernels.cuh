@@ -99,9 +99,9 @@ template <int P, int G = 0> struct Cfg;
 // G = 0: separable cell operator on affine meshes (two tiles per cell);
 // G = 1: general coefficient tensor per quadrature point (three tiles per cell, smaller bricks).
 MFCG_CFG(1, 0, 16, 16, 1, 256, 3, 2)
-MFCG_CFG(2, 0, 10, 10, 3, 192, 3, 2)
-MFCG_CFG(3, 0, 6, 6, 8, 224, 3, 2)
-MFCG_CFG(4, 0, 5, 5, 9, 288, 3, 2)
+MFCG_CFG(2, 0, 8, 8, 3, 256, 3, 2)
+MFCG_CFG(3, 0, 8, 4, 8, 256, 3, 2)
+MFCG_CFG(4, 0, 4, 4, 13, 288, 3, 2)
 #ifndef MFCG_KC5
 #define MFCG_KC5 3
 #endif
@@ -172,7 +172,7 @@ template <int P, int G = 0> struct Geo {
   // different banks in every sweep, whatever the line.  Needs a multiple of 16 cells per layer.
   static constexpr bool CELL_MINOR = (G == 0) && (NCELL % 16 == 0);
   // tile strides: element (k, j, i) of a cell tile sits at k*PSTR + j*RS + i.
-  //  - CELL_MINOR: dense rows; tile stride odd and = P mod 16 (then the gather, whose lanes walk
+  //  - CELL_MINOR: dense rows; tile stride odd and = P (P + 1 for even P) mod 16 (then the gather, whose lanes walk
   //    along x through consecutive cells, is conflict free as well)
   //  - otherwise: odd row stride (2-way conflicts in the y and z sweeps)
   static constexpr int RS = CELL_MINOR ? N : ((N % 2 == 0) ? N + 1 : N);
@@ -180,7 +180,7 @@ template <int P, int G = 0> struct Geo {
   static constexpr int tile_stride() {
     if (!CELL_MINOR) return N * PSTR;
     int t = N * PSTR;
-    while (t % 2 == 0 || t % 16 != P % 16) ++t;
+    while (t % 2 == 0 || t % 16 != (P | 1) % 16) ++t;
     return t;
   }
   static constexpr int TILE = tile_stride();
@@ -770,7 +770,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
     constexpr int TPC = Cfg<P, G>::TPC, LPT = (N * N + TPC - 1) / TPC;
     constexpr bool CM = Geo<P, G>::CELL_MINOR;
     const int cell = CM ? tid % NCELL : tid / TPC, q = CM ? tid / NCELL : tid - cell * TPC;
-    const bool has_cell = cell < bcx * bcy;
+    const bool has_cell = cell < bcx * bcy && q < TPC;  // padding lanes of the last warp own no lines
     const int cy = has_cell ? cell / bcx : 0, cx = has_cell ? cell - cy * bcx : 0;
     T* const At = A + cell * TILE;
     T* const Bt = Bs + cell * TILE;
