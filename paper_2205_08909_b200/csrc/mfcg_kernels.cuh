@@ -195,8 +195,14 @@ template <int P, int G = 0> struct Geo {
   }
   // separable path: table of the P^3 distinct 1/diag values of brick-interior DoFs (affine meshes)
   template <typename T> __host__ __device__ static constexpr size_t dtab_offset() { return red_offset<T>() + 8 * 7 * 32; }
-  template <typename T> __host__ __device__ static constexpr size_t smem_bytes() {
+  // separable path: per item of a layer's interior run (plane kk, row, column) the packed
+  // ring offset and 1/diag class, so the memory warps decode an item with one 32-bit load
+  static constexpr int ITAB_N = G == 0 ? P * (P * Cfg<P, G>::BX - 1) * (P * Cfg<P, G>::BY - 1) : 0;
+  template <typename T> __host__ __device__ static constexpr size_t itab_offset() {
     return dtab_offset<T>() + (G == 0 ? ((sizeof(T) * (size_t)(P * P * P) + 15) & ~(size_t)15) : 0);
+  }
+  template <typename T> __host__ __device__ static constexpr size_t smem_bytes() {
+    return itab_offset<T>() + ((4 * (size_t)ITAB_N + 15) & ~(size_t)15);
   }
 };
 
@@ -517,6 +523,9 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
   constexpr size_t RED_OFF = Geo<P, G>::template red_offset<T>();
   double* red = reinterpret_cast<double*>(smem_raw + RED_OFF);
   T* dtab = reinterpret_cast<T*>(smem_raw + Geo<P, G>::template dtab_offset<T>());
+  unsigned* itab = reinterpret_cast<unsigned*>(smem_raw + Geo<P, G>::template itab_offset<T>());
+  constexpr bool USE_ITAB = G == 0;
+  static_assert(!USE_ITAB || (PLANE < 1024 && P * P * P <= 512 && P < 8 + 1), "packed item table fields");
 
 #ifdef MFCG_TIMING
   __shared__ unsigned long long tcnt[16];
@@ -552,6 +561,17 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
   if (MODE == 1 && G == 0 && tab.diag_onfly)
     for (int i = tid; i < P * P * P; i += NT_C + NT_P)
       dtab[i] = diag_inverse_onfly<T, N>(tab, i % P, (i / P) % P, i / (P * P));
+  if (USE_ITAB) {
+    // item it = (kk * (Ly-1) + jm) * (Lx-1) + im of a layer's interior run: lattice plane Kfirst + kk
+    // with Kfirst = 1 (mod P), row jm + 1, column im + 1
+    const int lxm_ = Lx - 1, n2d_ = (Lx - 1) * (Ly - 1);
+    for (int it = tid; it < P * n2d_; it += NT_C + NT_P) {
+      const int kk = it / n2d_, rem2 = it - kk * n2d_, jm = rem2 / lxm_, im = rem2 - jm * lxm_;
+      const unsigned inplane = (unsigned)((jm + 1) * WX + im + 1);
+      const unsigned didx = (unsigned)((((1 + kk) % P) * P + (jm + 1) % P) * P + (im + 1) % P);
+      itab[it] = (unsigned)kk | (inplane << 4) | (didx << 14);
+    }
+  }
   __syncthreads();
 
   const int fw = Lx + 1, fp = fw * (Ly + 1);
@@ -569,8 +589,6 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
     const unsigned n2d_magic = nint2d > 0 ? (unsigned)((0x100000000ull + nint2d - 1) / nint2d) : 0u;
     const unsigned per_magic = (unsigned)((0x100000000ull + nperim - 1) / nperim);
     const i64 st_int = st27[13];
-    if (!ONCHIP && (ptid & 31) == 0)
-      for (int q = 0; q < 7; ++q) red[pwarp * 7 + q] = 0.0;
     // interior run of layer Lq in every vector: [run_first(Lq), +run_count(Lq))
     auto prefetch_layer = [&](int Lq) {
       if (Lq >= bcz || nint2d <= 0 || ptid >= 5) return;
@@ -598,6 +616,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
 #endif
     constexpr int PF = MFCG_L2_PREFETCH;
     for (int Lq = 0; Lq < PF; ++Lq) prefetch_layer(Lq);
+    double s[7] = {0, 0, 0, 0, 0, 0, 0};  // the thread's share of the seven sums over the whole brick
     MFCG_TIC(tp);
     for (int L = 0; L < bcz + 2; ++L) {
       const int stage = L & 1;
@@ -613,6 +632,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
         const int Klast = L * P + P < Lz - 1 ? L * P + P : Lz - 1;
         const int nitem = (nint2d > 0 && Klast >= Kfirst && !(MFCG_SKIP & 8)) ? (Klast - Kfirst + 1) * nint2d : 0;
         const i64 gbase = st_int + (i64)nint2d * (Kfirst - 1);
+        const int kslot = Kfirst % RB;
         for (int it0 = ptid; it0 < nitem; it0 += KC * NT_P) {
           T rr[KC], vv[KC], pp[KC], mm[KC], xx[KC];
 #pragma unroll
@@ -635,16 +655,23 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
           for (int c = 0; c < KC; ++c) {
             const int it = it0 + c * NT_P;
             if (it >= nitem) continue;
-            const int kk = (int)__umulhi((unsigned)it, n2d_magic);
-            const int rem2 = it - kk * nint2d;
-            const int jm = (int)(((unsigned)rem2 * lxm_magic) >> 16);
-            const int im = rem2 - jm * lxm;
-            MFCG_CHECK(kk >= 0 && Kfirst + kk <= Klast && jm >= 0 && jm < Ly - 1 && im >= 0 && im < Lx - 1);
+            int kk, inplane, didx = 0;
+            if (USE_ITAB) {
+              const unsigned e = itab[it];
+              kk = (int)(e & 15u); inplane = (int)((e >> 4) & 1023u); didx = (int)(e >> 14);
+            } else {
+              kk = (int)__umulhi((unsigned)it, n2d_magic);
+              const int rem2 = it - kk * nint2d;
+              const int jm = (int)(((unsigned)rem2 * lxm_magic) >> 16);
+              const int im = rem2 - jm * lxm;
+              inplane = (jm + 1) * WX + im + 1;
+            }
+            MFCG_CHECK(kk >= 0 && Kfirst + kk <= Klast && inplane > WX && inplane < PLANE);
             T val = pp[c];
             T rnew = (T)0;
             if (MODE == 1) {
               const i64 gi = gbase + it;
-              if (G == 0 && tab.diag_onfly) mm[c] = dtab[(((Kfirst + kk) % P) * P + (jm + 1) % P) * P + (im + 1) % P];
+              if (G == 0 && tab.diag_onfly) mm[c] = dtab[didx];
               T r = rr[c], p = pp[c];
               if (xmode) {
                 T x = xx[c];
@@ -659,7 +686,9 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
               val = p;
               rnew = r;
             }
-            const int rdst = ((Kfirst + kk) % RB) * PLANE + (jm + 1) * WX + im + 1;
+            int slot = kslot + kk;
+            if (slot >= RB) slot -= RB;
+            const int rdst = slot * PLANE + inplane;
             ring[rdst] = val;
             if (ONCHIP) { Rring[rdst] = rnew; Mring[rdst] = mm[c]; }
           }
@@ -726,7 +755,6 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
         const int Klo = Lp == 0 ? 1 : Lp * P, Khi = Lp * P + P - 1;
         const int nitem = nint2d > 0 ? (Khi - Klo + 1) * nint2d : 0;
         const i64 gbase = st_int + (i64)nint2d * (Klo - 1);
-        double s[7] = {0, 0, 0, 0, 0, 0, 0};
         for (int it0 = ptid; it0 < nitem; it0 += KC * NT_P) {
           T rr[KC], vv[KC], pp[KC], mm[KC];
 #pragma unroll
@@ -738,11 +766,9 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
               MFCG_CHECK(gi >= 0 && gi < n_int);
               rr[c] = R[gi]; vv[c] = V[gi]; pp[c] = Pv[gi];
               if (G == 0 && tab.diag_onfly) {
-                const int kk = (int)__umulhi((unsigned)it, n2d_magic);
-                const int rem2 = it - kk * nint2d;
-                const int jm = (int)(((unsigned)rem2 * lxm_magic) >> 16);
-                const int im = rem2 - jm * lxm;
-                mm[c] = dtab[(((Klo + kk) % P) * P + (jm + 1) % P) * P + (im + 1) % P];
+                // plane Klo + kk: the table is laid out for planes = 1 + kk (mod P)
+                const int itp = Lp == 0 ? it : (it >= nint2d ? it - nint2d : it + (P - 1) * nint2d);
+                mm[c] = dtab[itab[itp] >> 14];
               } else {
                 mm[c] = Minv[gi];
               }
@@ -756,12 +782,14 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             s[4] += r * mr; s[5] += r * mv; s[6] += v * mv;
           }
         }
-        warp_reduce7(s);
-        if ((ptid & 31) == 0)
-#pragma unroll
-          for (int q = 0; q < 7; ++q) red[pwarp * 7 + q] += s[q];
         MFCG_TOC(tp, 2);
       }
+    }
+    if (MODE == 1 && !ONCHIP) {  // one warp reduction per brick, not per layer
+      warp_reduce7(s);
+      if ((ptid & 31) == 0)
+#pragma unroll
+        for (int q = 0; q < 7; ++q) red[pwarp * 7 + q] = s[q];
     }
   } else {
     // ===================== math warps =====================
