@@ -201,8 +201,13 @@ template <int P, int G = 0> struct Geo {
   template <typename T> __host__ __device__ static constexpr size_t itab_offset() {
     return dtab_offset<T>() + (G == 0 ? ((sizeof(T) * (size_t)(P * P * P) + 15) & ~(size_t)15) : 0);
   }
-  template <typename T> __host__ __device__ static constexpr size_t smem_bytes() {
+  // separable path: one packed descriptor per lattice point of a layer for the gather
+  static constexpr int GTAB_N = G == 0 ? (P * Cfg<P, G>::BX + 1) * (P * Cfg<P, G>::BY + 1) : 0;
+  template <typename T> __host__ __device__ static constexpr size_t gtab_offset() {
     return itab_offset<T>() + ((4 * (size_t)ITAB_N + 15) & ~(size_t)15);
+  }
+  template <typename T> __host__ __device__ static constexpr size_t smem_bytes() {
+    return gtab_offset<T>() + 8 * (size_t)GTAB_N;
   }
 };
 
@@ -482,6 +487,20 @@ __device__ __forceinline__ void prefetch_l2_run(const T* ptr, i64 first, i64 cou
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr + lo), "r"(bytes) : "memory");
 }
 
+// -DMFCG_LEADER_POLL: one warp of a role polls the mbarrier, the role's other warps sleep in a
+// hardware named barrier.  Polling by every warp is 37 % of all issued instructions, yet the
+// leader variant measured 1.5 % slower (profiles/r01_notes.md), so every warp polls by default.
+template <int COUNT> __device__ __forceinline__ void role_wait(unsigned long long* bar, unsigned parity, bool leader, int id) {
+#ifndef MFCG_LEADER_POLL
+  mbar_wait(bar, parity);
+#else
+  if (leader) mbar_wait(bar, parity);
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(COUNT) : "memory");
+#endif
+}
+#ifndef MFCG_UNROLL_T
+#define MFCG_UNROLL_T 1
+#endif
 template <int COUNT> __device__ __forceinline__ void math_barrier() {
   asm volatile("bar.sync 1, %0;" ::"n"(COUNT) : "memory");
 }
@@ -525,6 +544,8 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
   T* dtab = reinterpret_cast<T*>(smem_raw + Geo<P, G>::template dtab_offset<T>());
   unsigned* itab = reinterpret_cast<unsigned*>(smem_raw + Geo<P, G>::template itab_offset<T>());
   constexpr bool USE_ITAB = G == 0;
+  uint2* gtab = reinterpret_cast<uint2*>(smem_raw + Geo<P, G>::template gtab_offset<T>());
+  constexpr bool USE_GTAB = G == 0;
   static_assert(!USE_ITAB || (PLANE < 1024 && P * P * P <= 512 && P < 8 + 1), "packed item table fields");
 
 #ifdef MFCG_TIMING
@@ -561,6 +582,41 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
   if (MODE == 1 && G == 0 && tab.diag_onfly)
     for (int i = tid; i < P * P * P; i += NT_C + NT_P)
       dtab[i] = diag_inverse_onfly<T, N>(tab, i % P, (i / P) % P, i / (P * P));
+  // Gather descriptor of lattice point rem = j * (Lx+1) + i of a layer (independent of the layer):
+  //  x: tile offset of the point in cell (i/P, j/P) [13 bits], which of the four cells around it
+  //     exist (bits 13-16: (cx,cy), (cx-1,cy), (cx,cy-1), (cx-1,cy-1)), brick-boundary flag, entity
+  //  y: offset in the lattice plane, offset inside the macro entity, plane-stride selector
+  auto gather_descriptor = [&](int rem) -> uint2 {
+    const int fw_ = Lx + 1;
+    const int j = rem / fw_, i = rem - j * fw_;
+    const int ex = i == 0 ? 0 : (i == Lx ? 2 : 1), ey = j == 0 ? 0 : (j == Ly ? 2 : 1);
+    const int ox = ex == 1 ? i - 1 : 0, oy = ey == 1 ? j - 1 : 0;
+    const int lx = ex == 1 ? Lx - 1 : 1;
+    const int cx1 = i / P, ix1 = i - cx1 * P, cy1 = j / P, iy1 = j - cy1 * P;
+    const unsigned base = (unsigned)((cy1 * bcx + cx1) * TILE + iy1 * RS + ix1);
+    const unsigned v11 = cx1 < bcx && cy1 < bcy, v10 = ix1 == 0 && cx1 > 0 && cy1 < bcy,
+                   v01 = iy1 == 0 && cy1 > 0 && cx1 < bcx, v00 = ix1 == 0 && iy1 == 0 && cx1 > 0 && cy1 > 0;
+    const unsigned edge = (ex != 1) || (ey != 1);
+    const unsigned sel = (ex == 1 ? 1u : 0u) | (ey == 1 ? 2u : 0u);
+    uint2 d;
+    d.x = base | (v11 << 13) | (v10 << 14) | (v01 << 15) | (v00 << 16) | (edge << 17) | ((unsigned)(ex + 3 * ey) << 18);
+    d.y = (unsigned)(j * WX + i) | ((unsigned)(ox + lx * oy) << 10) | (sel << 22);
+    return d;
+  };
+  if (USE_GTAB) {
+    // table order: first the points strictly inside a cell in x and y (one contribution, plain
+    // stores: warps of the gather stay uniform), then the cell-boundary points
+    const int fw_ = Lx + 1, rowc = bcx * (P - 1), n_in = rowc * bcy * (P - 1);
+    for (int rem = tid; rem < fw_ * (Ly + 1); rem += NT_C + NT_P) {
+      const int j = rem / fw_, i = rem - j * fw_;
+      const int cx1 = i / P, ix1 = i - cx1 * P, cy1 = j / P, iy1 = j - cy1 * P;
+      const int rows_before = cy1 * (P - 1) + (iy1 == 0 ? 0 : iy1 - 1);
+      const int in_row_before = cx1 * (P - 1) + (ix1 == 0 ? 0 : ix1 - 1);
+      const bool inner = ix1 != 0 && iy1 != 0;
+      const int before = rows_before * rowc + (iy1 != 0 ? in_row_before : 0);  // inner points with smaller rem
+      gtab[inner ? before : n_in + rem - before] = gather_descriptor(rem);
+    }
+  }
   if (USE_ITAB) {
     // item it = (kk * (Ly-1) + jm) * (Lx-1) + im of a layer's interior run: lattice plane Kfirst + kk
     // with Kfirst = 1 (mod P), row jm + 1, column im + 1
@@ -575,7 +631,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
   __syncthreads();
 
   const int fw = Lx + 1, fp = fw * (Ly + 1);
-  const unsigned fw_magic = (65536u + fw - 1) / fw;
+  const int nint2d_c = (Lx - 1) * (Ly - 1);  // interior points of one lattice plane
   const i64 n_int = g.n_int;
 
   if (tid >= NT_C) {
@@ -622,7 +678,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
       const int stage = L & 1;
       if (PF > 0) prefetch_layer(L + PF);
       // the ring planes layer L overwrites were last read by the x sweep of layer L-2
-      if (L >= 2 && L < bcz) mbar_wait(&bars[2 + stage], ((L >> 1) - 1) & 1);
+      if (L >= 2 && L < bcz) role_wait<NT_P>(&bars[2 + stage], ((L >> 1) - 1) & 1, pwarp == 0, 2);
       MFCG_TOC(tp, 0);
       if (L < bcz) {
         // ---- fill the ring with the planes layer L adds (plane 0 is shared with layer L-1)
@@ -748,7 +804,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
         MFCG_TOC(tp, 1);
       }
       if (MODE == 1 && !ONCHIP && L >= 2 && !(MFCG_SKIP & 4)) {
-        mbar_wait(&bars[4 + stage], ((L >> 1) - 1) & 1);  // v of layer L-2 stored
+        role_wait<NT_P>(&bars[4 + stage], ((L >> 1) - 1) & 1, pwarp == 0, 2);  // v of layer L-2 stored
         // ---- post sums of layer L-2 (solvers.py:692-698): its v is final and, like r, p and
         // 1/diag, still resident in L2; one contiguous run per vector
         const int Lp = L - 2;
@@ -797,6 +853,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
     // that cell in every sweep of every layer, so all index arithmetic is hoisted.
     constexpr int TPC = Cfg<P, G>::TPC, LPT = (N * N + TPC - 1) / TPC;
     constexpr bool CM = Geo<P, G>::CELL_MINOR;
+    constexpr int UNROLL_T = MFCG_UNROLL_T;  // lines of a sweep in flight per thread
     const int cell = CM ? tid % NCELL : tid / TPC, q = CM ? tid / NCELL : tid - cell * TPC;
     const bool has_cell = cell < bcx * bcy && q < TPC;  // padding lanes of the last warp own no lines
     const int cy = has_cell ? cell / bcx : 0, cx = has_cell ? cell - cy * bcx : 0;
@@ -809,8 +866,14 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
     for (int L = 0; L < bcz; ++L) {
       const int stage = L & 1;
       const int s0 = (L * P) % RB;
+#ifndef MFCG_LEADER_POLL
       if (L > 0) math_barrier<NT_C>();        // every math thread is done with the previous gather's tiles
       mbar_wait(&bars[stage], (L >> 1) & 1);  // layer L full
+#else
+      // layer L full; the barrier also says every math thread is done with the previous gather's tiles
+      if (tid < 32) mbar_wait(&bars[stage], (L >> 1) & 1);
+      math_barrier<NT_C>();
+#endif
       MFCG_TOC(tc, 4);
 
       if (G >= 1) {
@@ -983,7 +1046,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
       } else {
         // ---- x sweep: a = M u, b = gx K u along every x line of the cell
         if (has_cell && !(MFCG_SKIP & 1)) {
-  #pragma unroll 1
+  #pragma unroll UNROLL_T
           for (int t = 0; t < LPT; ++t) {
             const int l = LineOrder<N>::x(q + t * TPC, TPC);
             if (l < 0) continue;
@@ -1019,7 +1082,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
 
         // ---- y sweep (in place): c = M a, de = gy K a + M b
         if (has_cell && !(MFCG_SKIP & 1)) {
-  #pragma unroll 1
+  #pragma unroll UNROLL_T
           for (int t = 0; t < LPT; ++t) {
             const int l = LineOrder<N>::y(q + t * TPC, TPC);
             if (l < 0) continue;
@@ -1055,7 +1118,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
 
         // ---- z sweep: out = M de + gz K c, written over c
         if (has_cell && !(MFCG_SKIP & 1)) {
-  #pragma unroll 1
+  #pragma unroll UNROLL_T
           for (int t = 0; t < LPT; ++t) {
             const int l = LineOrder<N>::z(q + t * TPC, TPC);
             if (l < 0) continue;
@@ -1088,26 +1151,36 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
       // ---- gather the cells' contributions per lattice point, finish the planes
       double s[7] = {0, 0, 0, 0, 0, 0, 0};
       for (int rem = tid; rem < ((MFCG_SKIP & 2) ? 0 : fp); rem += NT_C) {
-        const int j = (int)(((unsigned)rem * fw_magic) >> 16);
-        const int i = rem - j * fw;
-        const int ex = i == 0 ? 0 : (i == Lx ? 2 : 1), ey = j == 0 ? 0 : (j == Ly ? 2 : 1);
-        const int ox = ex == 1 ? i - 1 : 0, oy = ey == 1 ? j - 1 : 0;
-        const int lx = ex == 1 ? Lx - 1 : 1, ly = ey == 1 ? Ly - 1 : 1;
-        const bool edge = (ex != 1) || (ey != 1);
-        const int e2 = ex + 3 * ey, o2 = ox + lx * oy, pstride = lx * ly;
-        int cx1 = i / P;
-        const int ix1 = i - cx1 * P;
-        const int cx0 = (ix1 == 0 && cx1 > 0) ? cx1 - 1 : -1;
-        if (cx1 >= bcx) cx1 = -1;
-        int cy1 = j / P;
-        const int iy1 = j - cy1 * P;
-        const int cy0 = (iy1 == 0 && cy1 > 0) ? cy1 - 1 : -1;
-        if (cy1 >= bcy) cy1 = -1;
+        const uint2 d = USE_GTAB ? gtab[rem] : gather_descriptor(rem);
+        const int base = (int)(d.x & 8191u), cw = (int)(d.y & 1023u), o2 = (int)((d.y >> 10) & 4095u);
+        if (!ONCHIP && ((d.x >> 13) & 31u) == 1u) {
+          // strictly inside one cell in x and y: one contribution per plane, brick-interior DoFs
+          const T* a = A + base;
+          const i64 gi0 = st27[13] + o2 + (i64)nint2d_c * (L * P - 1);
+          MFCG_CHECK(base + P * PSTR < NCELL * TILE && cw < PLANE);
+          {
+            const T sum = a[0] + carry[cw];
+            if (L == 0) atomicAdd(&V[st27[4] + o2], sum);  // the brick's bottom face is shared
+            else { MFCG_CHECK(gi0 >= 0 && gi0 < n_int); V[gi0] = sum; }
+          }
+#pragma unroll
+          for (int k = 1; k < P; ++k) {
+            MFCG_CHECK(gi0 + (i64)k * nint2d_c >= 0 && gi0 + (i64)k * nint2d_c < n_int);
+            V[gi0 + (i64)k * nint2d_c] = a[k * PSTR];
+          }
+          if (L < bcz - 1) carry[cw] = a[P * PSTR];
+          else atomicAdd(&V[st27[22] + o2], a[P * PSTR]);  // top face
+          continue;
+        }
+        const bool edge = (d.x >> 17) & 1u;
+        const int e2 = (int)((d.x >> 18) & 15u);
+        const unsigned sel = d.y >> 22;
+        const int pstride = ((sel & 1u) ? Lx - 1 : 1) * ((sel & 2u) ? Ly - 1 : 1);
         // offsets of the (up to four) cell-tile entries holding this point
-        const int o11 = (cy1 >= 0 && cx1 >= 0) ? (cy1 * bcx + cx1) * TILE + iy1 * RS + ix1 : -1;
-        const int o10 = (cy1 >= 0 && cx0 >= 0) ? (cy1 * bcx + cx0) * TILE + iy1 * RS + P : -1;
-        const int o01 = (cy0 >= 0 && cx1 >= 0) ? (cy0 * bcx + cx1) * TILE + P * RS + ix1 : -1;
-        const int o00 = (cy0 >= 0 && cx0 >= 0) ? (cy0 * bcx + cx0) * TILE + P * RS + P : -1;
+        const int o11 = (d.x & (1u << 13)) ? base : -1;
+        const int o10 = (d.x & (1u << 14)) ? base - TILE + P : -1;
+        const int o01 = (d.x & (1u << 15)) ? base - bcx * TILE + P * RS : -1;
+        const int o00 = (d.x & (1u << 16)) ? base - (bcx + 1) * TILE + P * RS + P : -1;
 #pragma unroll
         for (int k = 0; k <= P; ++k) {
           T sum = 0;
@@ -1115,9 +1188,9 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
           if (o01 >= 0) sum += A[o01 + k * PSTR];
           if (o10 >= 0) sum += A[o10 + k * PSTR];
           if (o11 >= 0) sum += A[o11 + k * PSTR];
-          if (k == 0) sum += carry[j * WX + i];
+          if (k == 0) sum += carry[cw];
           if (k == P && L < bcz - 1) {
-            carry[j * WX + i] = sum;
+            carry[cw] = sum;
             continue;
           }
           const int K = L * P + k;
@@ -1131,7 +1204,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             if (ONCHIP) {  // post on values that never left the SM (solvers.py:692-698)
               int slot = s0 + k;
               if (slot >= RB) slot -= RB;
-              const int ro = slot * PLANE + j * WX + i;
+              const int ro = slot * PLANE + cw;
               const double r = (double)Rring[ro], m = (double)Mring[ro], p = (double)ring[ro], v = (double)sum;
               const double mr = m * r, mv = m * v;
               s[0] += r * r; s[1] += p * v; s[2] += r * v; s[3] += v * v;
