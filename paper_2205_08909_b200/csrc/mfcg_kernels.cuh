@@ -605,16 +605,23 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
   };
   if (USE_GTAB) {
     // table order: first the points strictly inside a cell in x and y (one contribution, plain
-    // stores: warps of the gather stay uniform), then the cell-boundary points
+    // stores: warps of the gather stay uniform), then the brick-boundary points in the perimeter
+    // order of the memory warps (which read the same descriptors), then the other cell-boundary points
     const int fw_ = Lx + 1, rowc = bcx * (P - 1), n_in = rowc * bcy * (P - 1);
+    const int nper = 2 * fw_ + 2 * (Ly - 1);
     for (int rem = tid; rem < fw_ * (Ly + 1); rem += NT_C + NT_P) {
       const int j = rem / fw_, i = rem - j * fw_;
       const int cx1 = i / P, ix1 = i - cx1 * P, cy1 = j / P, iy1 = j - cy1 * P;
       const int rows_before = cy1 * (P - 1) + (iy1 == 0 ? 0 : iy1 - 1);
       const int in_row_before = cx1 * (P - 1) + (ix1 == 0 ? 0 : ix1 - 1);
-      const bool inner = ix1 != 0 && iy1 != 0;
       const int before = rows_before * rowc + (iy1 != 0 ? in_row_before : 0);  // inner points with smaller rem
-      gtab[inner ? before : n_in + rem - before] = gather_descriptor(rem);
+      int pos;
+      if (ix1 != 0 && iy1 != 0) pos = before;
+      else if (j == 0) pos = n_in + i;
+      else if (j == Ly) pos = n_in + fw_ + i;
+      else if (i == 0 || i == Lx) pos = n_in + 2 * fw_ + 2 * (j - 1) + (i == Lx ? 1 : 0);
+      else pos = n_in + nper + (rem - before - (fw_ + 2 * (j - 1) + 1));
+      gtab[pos] = gather_descriptor(rem);
     }
   }
   if (USE_ITAB) {
@@ -632,6 +639,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
 
   const int fw = Lx + 1, fp = fw * (Ly + 1);
   const int nint2d_c = (Lx - 1) * (Ly - 1);  // interior points of one lattice plane
+  const int n_in_c = bcx * (P - 1) * bcy * (P - 1);  // lattice points of a plane strictly inside a cell
   const i64 n_int = g.n_int;
 
   if (tid >= NT_C) {
@@ -764,20 +772,29 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
               if (it < nsh) {
                 const int kk = (int)__umulhi((unsigned)it, per_magic);
                 const int e = it - kk * nperim;
-                int i, j;
-                if (e < fw) { j = 0; i = e; }
-                else if (e < 2 * fw) { j = Ly; i = e - fw; }
-                else { const int r2 = e - 2 * fw; j = 1 + (r2 >> 1); i = (r2 & 1) ? Lx : 0; }
-                const int ex = i == 0 ? 0 : (i == Lx ? 2 : 1), ey = j == 0 ? 0 : (j == Ly ? 2 : 1);
-                const int ox = ex == 1 ? i - 1 : 0, oy = ey == 1 ? j - 1 : 0;
-                const int lx = ex == 1 ? Lx - 1 : 1, ly = ey == 1 ? Ly - 1 : 1;
+                int e2, o2, cw, pstride;
+                if (USE_GTAB) {
+                  const uint2 d = gtab[n_in_c + e];
+                  e2 = (int)((d.x >> 18) & 15u); cw = (int)(d.y & 1023u); o2 = (int)((d.y >> 10) & 4095u);
+                  const unsigned sel = d.y >> 22;
+                  pstride = ((sel & 1u) ? Lx - 1 : 1) * ((sel & 2u) ? Ly - 1 : 1);
+                } else {
+                  int i, j;
+                  if (e < fw) { j = 0; i = e; }
+                  else if (e < 2 * fw) { j = Ly; i = e - fw; }
+                  else { const int r2 = e - 2 * fw; j = 1 + (r2 >> 1); i = (r2 & 1) ? Lx : 0; }
+                  const int ex = i == 0 ? 0 : (i == Lx ? 2 : 1), ey = j == 0 ? 0 : (j == Ly ? 2 : 1);
+                  const int ox = ex == 1 ? i - 1 : 0, oy = ey == 1 ? j - 1 : 0;
+                  const int lx = ex == 1 ? Lx - 1 : 1, ly = ey == 1 ? Ly - 1 : 1;
+                  e2 = ex + 3 * ey; o2 = ox + lx * oy; cw = j * WX + i; pstride = lx * ly;
+                }
                 const int K = L * P + k0 + kk;
                 const int ez = K == 0 ? 0 : (K == Lz ? 2 : 1);
-                const i64 gi = st27[ex + 3 * ey + 9 * ez] + ox + lx * oy + (ez == 1 ? (i64)(lx * ly) * (K - 1) : 0);
-                MFCG_CHECK(gi >= n_int && gi < g.n_dofs && i >= 0 && i <= Lx && j >= 0 && j <= Ly && K >= 0 && K <= Lz);
+                const i64 gi = st27[e2 + 9 * ez] + o2 + (ez == 1 ? (i64)pstride * (K - 1) : 0);
+                MFCG_CHECK(gi >= n_int && gi < g.n_dofs && cw >= 0 && cw < PLANE && K >= 0 && K <= Lz);
                 pp[c] = MODE == 0 ? src[gi] : Pv[gi];
                 mk[c] = g.mask[gi - n_int] & 1;
-                dst[c] = (K % RB) * PLANE + j * WX + i;
+                dst[c] = (K % RB) * PLANE + cw;
               }
             }
 #pragma unroll
