@@ -680,7 +680,12 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
 #endif
     constexpr int PF = MFCG_L2_PREFETCH;
     for (int Lq = 0; Lq < PF; ++Lq) prefetch_layer(Lq);
-    double s[7] = {0, 0, 0, 0, 0, 0, 0};  // the thread's share of the seven sums over the whole brick
+    // separable path: the thread's share of the seven sums stays in registers over the whole brick;
+    // the curved paths (register-bound math warps) reduce per layer into the shared-memory slots
+    constexpr bool PER_BRICK_SUMS = G == 0;
+    double s[7] = {0, 0, 0, 0, 0, 0, 0};
+    if (!PER_BRICK_SUMS && !ONCHIP && (ptid & 31) == 0)
+      for (int q = 0; q < 7; ++q) red[pwarp * 7 + q] = 0.0;
     MFCG_TIC(tp);
     for (int L = 0; L < bcz + 2; ++L) {
       const int stage = L & 1;
@@ -855,10 +860,18 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             s[4] += r * mr; s[5] += r * mv; s[6] += v * mv;
           }
         }
+        if (!PER_BRICK_SUMS) {
+          warp_reduce7(s);
+          if ((ptid & 31) == 0)
+#pragma unroll
+            for (int q = 0; q < 7; ++q) red[pwarp * 7 + q] += s[q];
+#pragma unroll
+          for (int q = 0; q < 7; ++q) s[q] = 0.0;
+        }
         MFCG_TOC(tp, 2);
       }
     }
-    if (MODE == 1 && !ONCHIP) {  // one warp reduction per brick, not per layer
+    if (MODE == 1 && !ONCHIP && PER_BRICK_SUMS) {  // one warp reduction per brick, not per layer
       warp_reduce7(s);
       if ((ptid & 31) == 0)
 #pragma unroll
@@ -872,7 +885,8 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
     constexpr bool CM = Geo<P, G>::CELL_MINOR;
     constexpr int UNROLL_T = MFCG_UNROLL_T;  // lines of a sweep in flight per thread
     const int cell = CM ? tid % NCELL : tid / TPC, q = CM ? tid / NCELL : tid - cell * TPC;
-    const bool has_cell = cell < bcx * bcy && q < TPC;  // padding lanes of the last warp own no lines
+    // cell-minor: the padding lanes of the last warp own no lines (cell-major: q < TPC by construction)
+    const bool has_cell = cell < bcx * bcy && (!CM || q < TPC);
     const int cy = has_cell ? cell / bcx : 0, cx = has_cell ? cell - cy * bcx : 0;
     T* const At = A + cell * TILE;
     T* const Bt = Bs + cell * TILE;
