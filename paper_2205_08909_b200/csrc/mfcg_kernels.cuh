@@ -133,7 +133,7 @@ MFCG_CFG(1, 1, 16, 16, 1, 256, 3, 2)
 MFCG_CFG(2, 1, 10, 10, 3, 192, 3, 2)
 MFCG_CFG(3, 1, 6, 6, 8, 224, 3, 2)
 MFCG_CFG(4, 1, 5, 5, 9, 288, 3, 2)
-MFCG_CFG(5, 1, 4, 3, 12, 224, 3, 2)
+MFCG_CFG(5, 1, 4, 3, 18, 128, 3, 2)
 MFCG_CFG(6, 1, 3, 2, 25, 224, 3, 2)
 MFCG_CFG(7, 1, 2, 2, 32, 256, 3, 2)
 MFCG_CFG(8, 1, 2, 2, 32, 256, 3, 2)
@@ -501,6 +501,9 @@ template <int COUNT> __device__ __forceinline__ void role_wait(unsigned long lon
 #ifndef MFCG_UNROLL_T
 #define MFCG_UNROLL_T 1
 #endif
+#ifndef MFCG_GEO_PREFETCH
+#define MFCG_GEO_PREFETCH 0  // bulk L2 prefetch of the next layer's stored geometry (curved meshes)
+#endif
 template <int COUNT> __device__ __forceinline__ void math_barrier() {
   asm volatile("bar.sync 1, %0;" ::"n"(COUNT) : "memory");
 }
@@ -655,6 +658,20 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
     const i64 st_int = st27[13];
     // interior run of layer Lq in every vector: [run_first(Lq), +run_count(Lq))
     auto prefetch_layer = [&](int Lq) {
+#if MFCG_GEO_PREFETCH
+      // stored geometry of the layer's cells (one contiguous block per cell), read by the math warps
+      if (G == 1 && Lq < bcz && ptid >= 32 && ptid < 32 + bcx * bcy) {
+        const int c = ptid - 32, cy = c / bcx, cx = c - cy * bcx;
+        const i64 cellg = ((i64)(mz * g.B[2] + Lq) * g.cells[1] + (my * g.B[1] + cy)) * g.cells[0] + (mx * g.B[0] + cx);
+        constexpr int NQ3 = N * N * N;
+        const unsigned per = geo.kind == 1 ? 6u : 9u;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const T*>(geo.data) + cellg * NQ3 * per),
+                     "r"((unsigned)(NQ3 * per * sizeof(T))) : "memory");
+        if (geo.kind == 2)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const T*>(geo.jxw) + cellg * NQ3),
+                       "r"((unsigned)(NQ3 * sizeof(T))) : "memory");
+      }
+#endif
       if (Lq >= bcz || nint2d <= 0 || ptid >= 5) return;
       const int kq0 = Lq == 0 ? 0 : 1;
       const int Kf = Lq * P + kq0 > 1 ? Lq * P + kq0 : 1;
