@@ -501,6 +501,17 @@ template <int COUNT> __device__ __forceinline__ void role_wait(unsigned long lon
 #ifndef MFCG_UNROLL_T
 #define MFCG_UNROLL_T 1
 #endif
+// how the memory warps load the interior runs: 0 plain, 1 ld.global.cg (L2 only), 2 ld.global.cs (streaming)
+#ifndef MFCG_LOAD_HINT
+#define MFCG_LOAD_HINT 0
+#endif
+#if MFCG_LOAD_HINT == 1
+#define MFCG_LDG(p) __ldcg(p)
+#elif MFCG_LOAD_HINT == 2
+#define MFCG_LDG(p) __ldcs(p)
+#else
+#define MFCG_LDG(p) (*(p))
+#endif
 #ifndef MFCG_GEO_PREFETCH
 #define MFCG_GEO_PREFETCH 0  // bulk L2 prefetch of the next layer's stored geometry (curved meshes)
 #endif
@@ -731,9 +742,9 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
               if (MODE == 0) {
                 pp[c] = src[gi];
               } else {
-                pp[c] = Pv[gi]; rr[c] = R[gi]; vv[c] = V[gi];
-                if (!tab.diag_onfly) mm[c] = Minv[gi];
-                if (xmode) xx[c] = X[gi];
+                pp[c] = MFCG_LDG(Pv + gi); rr[c] = MFCG_LDG(R + gi); vv[c] = MFCG_LDG(V + gi);
+                if (!tab.diag_onfly) mm[c] = MFCG_LDG(Minv + gi);
+                if (xmode) xx[c] = MFCG_LDG(X + gi);
               }
             }
           }
@@ -859,7 +870,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             if (it < nitem) {
               const i64 gi = gbase + it;
               MFCG_CHECK(gi >= 0 && gi < n_int);
-              rr[c] = R[gi]; vv[c] = V[gi]; pp[c] = Pv[gi];
+              rr[c] = MFCG_LDG(R + gi); vv[c] = MFCG_LDG(V + gi); pp[c] = MFCG_LDG(Pv + gi);
               if (G == 0 && tab.diag_onfly) {
                 // plane Klo + kk: the table is laid out for planes = 1 + kk (mod P)
                 const int itp = Lp == 0 ? it : (it >= nint2d ? it - nint2d : it + (P - 1) * nint2d);
