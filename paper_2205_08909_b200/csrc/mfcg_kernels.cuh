@@ -28,9 +28,9 @@
 // a violation traps, which the host sees as a CUDA error.  (compute-sanitizer is closed on the
 // GPU pool this was developed on.)
 #ifdef MFCG_BOUNDS
-#define MFCG_CHECK(cond) do { if (!(cond)) __trap(); } while (0)
+#define MFCG_CHECK(...) do { if (!(__VA_ARGS__)) __trap(); } while (0)
 #else
-#define MFCG_CHECK(cond)
+#define MFCG_CHECK(...)
 #endif
 
 namespace mfcg {
@@ -635,6 +635,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
       else if (j == Ly) pos = n_in + fw_ + i;
       else if (i == 0 || i == Lx) pos = n_in + 2 * fw_ + 2 * (j - 1) + (i == Lx ? 1 : 0);
       else pos = n_in + nper + (rem - before - (fw_ + 2 * (j - 1) + 1));
+      MFCG_CHECK(pos >= 0 && pos < Geo<P, G>::GTAB_N);
       gtab[pos] = gather_descriptor(rem);
     }
   }
@@ -646,6 +647,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
       const int kk = it / n2d_, rem2 = it - kk * n2d_, jm = rem2 / lxm_, im = rem2 - jm * lxm_;
       const unsigned inplane = (unsigned)((jm + 1) * WX + im + 1);
       const unsigned didx = (unsigned)((((1 + kk) % P) * P + (jm + 1) % P) * P + (im + 1) % P);
+      MFCG_CHECK(it < Geo<P, G>::ITAB_N && inplane < 1024u && didx < (unsigned)(P * P * P));
       itab[it] = (unsigned)kk | (inplane << 4) | (didx << 14);
     }
   }
@@ -754,6 +756,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             if (it >= nitem) continue;
             int kk, inplane, didx = 0;
             if (USE_ITAB) {
+              MFCG_CHECK(it >= 0 && it < Geo<P, G>::ITAB_N);
               const unsigned e = itab[it];
               kk = (int)(e & 15u); inplane = (int)((e >> 4) & 1023u); didx = (int)(e >> 14);
             } else {
@@ -807,6 +810,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
                 const int e = it - kk * nperim;
                 int e2, o2, cw, pstride;
                 if (USE_GTAB) {
+                  MFCG_CHECK(e >= 0 && n_in_c + e < Geo<P, G>::GTAB_N);
                   const uint2 d = gtab[n_in_c + e];
                   e2 = (int)((d.x >> 18) & 15u); cw = (int)(d.y & 1023u); o2 = (int)((d.y >> 10) & 4095u);
                   const unsigned sel = d.y >> 22;
@@ -874,6 +878,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
               if (G == 0 && tab.diag_onfly) {
                 // plane Klo + kk: the table is laid out for planes = 1 + kk (mod P)
                 const int itp = Lp == 0 ? it : (it >= nint2d ? it - nint2d : it + (P - 1) * nint2d);
+                MFCG_CHECK(itp >= 0 && itp < Geo<P, G>::ITAB_N && (itab[itp] >> 14) < (unsigned)(P * P * P));
                 mm[c] = dtab[itab[itp] >> 14];
               } else {
                 mm[c] = Minv[gi];
@@ -1210,6 +1215,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
       // ---- gather the cells' contributions per lattice point, finish the planes
       double s[7] = {0, 0, 0, 0, 0, 0, 0};
       for (int rem = tid; rem < ((MFCG_SKIP & 2) ? 0 : fp); rem += NT_C) {
+        MFCG_CHECK(!USE_GTAB || rem < Geo<P, G>::GTAB_N);
         const uint2 d = USE_GTAB ? gtab[rem] : gather_descriptor(rem);
         const int base = (int)(d.x & 8191u), cw = (int)(d.y & 1023u), o2 = (int)((d.y >> 10) & 4095u);
         if (!ONCHIP && ((d.x >> 13) & 31u) == 1u) {
