@@ -111,6 +111,13 @@ MFCG_CFG(4, 0, 4, 4, 13, 288, 3, 2)
 #ifndef MFCG_NTP5
 #define MFCG_NTP5 320
 #endif
+#ifndef MFCG_BX5
+#define MFCG_BX5 4
+#define MFCG_BY5 4
+#endif
+#ifndef MFCG_MINB5
+#define MFCG_MINB5 2
+#endif
 #ifndef MFCG_V7
 #define MFCG_V7 0
 #endif
@@ -124,7 +131,7 @@ MFCG_CFG(4, 0, 4, 4, 13, 288, 3, 2)
 #endif
 MFCG_CFG_X(5, 0, MFCG_V7_BX, MFCG_V7_BY, MFCG_TPC5, MFCG_NTP5, MFCG_KC5, MFCG_V7_MINB, true)
 #else
-MFCG_CFG(5, 0, 4, 4, MFCG_TPC5, MFCG_NTP5, MFCG_KC5, 2)
+MFCG_CFG_X(5, 0, MFCG_BX5, MFCG_BY5, MFCG_TPC5, MFCG_NTP5, MFCG_KC5, MFCG_MINB5, false)
 #endif
 MFCG_CFG(6, 0, 3, 3, 25, 256, 3, 2)
 MFCG_CFG(7, 0, 2, 2, 32, 256, 3, 2)
@@ -597,8 +604,8 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
     for (int i = tid; i < P * P * P; i += NT_C + NT_P)
       dtab[i] = diag_inverse_onfly<T, N>(tab, i % P, (i / P) % P, i / (P * P));
   // Gather descriptor of lattice point rem = j * (Lx+1) + i of a layer (independent of the layer):
-  //  x: tile offset of the point in cell (i/P, j/P) [13 bits], which of the four cells around it
-  //     exist (bits 13-16: (cx,cy), (cx-1,cy), (cx,cy-1), (cx-1,cy-1)), brick-boundary flag, entity
+  //  x: tile offset of the point in cell (i/P, j/P) [14 bits], which of the four cells around it
+  //     exist (bits 14-17: (cx,cy), (cx-1,cy), (cx,cy-1), (cx-1,cy-1)), brick-boundary flag, entity
   //  y: offset in the lattice plane, offset inside the macro entity, plane-stride selector
   auto gather_descriptor = [&](int rem) -> uint2 {
     const int fw_ = Lx + 1;
@@ -613,7 +620,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
     const unsigned edge = (ex != 1) || (ey != 1);
     const unsigned sel = (ex == 1 ? 1u : 0u) | (ey == 1 ? 2u : 0u);
     uint2 d;
-    d.x = base | (v11 << 13) | (v10 << 14) | (v01 << 15) | (v00 << 16) | (edge << 17) | ((unsigned)(ex + 3 * ey) << 18);
+    d.x = base | (v11 << 14) | (v10 << 15) | (v01 << 16) | (v00 << 17) | (edge << 18) | ((unsigned)(ex + 3 * ey) << 19);
     d.y = (unsigned)(j * WX + i) | ((unsigned)(ox + lx * oy) << 10) | (sel << 22);
     return d;
   };
@@ -812,7 +819,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
                 if (USE_GTAB) {
                   MFCG_CHECK(e >= 0 && n_in_c + e < Geo<P, G>::GTAB_N);
                   const uint2 d = gtab[n_in_c + e];
-                  e2 = (int)((d.x >> 18) & 15u); cw = (int)(d.y & 1023u); o2 = (int)((d.y >> 10) & 4095u);
+                  e2 = (int)((d.x >> 19) & 15u); cw = (int)(d.y & 1023u); o2 = (int)((d.y >> 10) & 4095u);
                   const unsigned sel = d.y >> 22;
                   pstride = ((sel & 1u) ? Lx - 1 : 1) * ((sel & 2u) ? Ly - 1 : 1);
                 } else {
@@ -1217,8 +1224,8 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
       for (int rem = tid; rem < ((MFCG_SKIP & 2) ? 0 : fp); rem += NT_C) {
         MFCG_CHECK(!USE_GTAB || rem < Geo<P, G>::GTAB_N);
         const uint2 d = USE_GTAB ? gtab[rem] : gather_descriptor(rem);
-        const int base = (int)(d.x & 8191u), cw = (int)(d.y & 1023u), o2 = (int)((d.y >> 10) & 4095u);
-        if (!ONCHIP && ((d.x >> 13) & 31u) == 1u) {
+        const int base = (int)(d.x & 16383u), cw = (int)(d.y & 1023u), o2 = (int)((d.y >> 10) & 4095u);
+        if (!ONCHIP && ((d.x >> 14) & 31u) == 1u) {
           // strictly inside one cell in x and y: one contribution per plane, brick-interior DoFs
           const T* a = A + base;
           const i64 gi0 = st27[13] + o2 + (i64)nint2d_c * (L * P - 1);
@@ -1237,15 +1244,15 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
           else atomicAdd(&V[st27[22] + o2], a[P * PSTR]);  // top face
           continue;
         }
-        const bool edge = (d.x >> 17) & 1u;
-        const int e2 = (int)((d.x >> 18) & 15u);
+        const bool edge = (d.x >> 18) & 1u;
+        const int e2 = (int)((d.x >> 19) & 15u);
         const unsigned sel = d.y >> 22;
         const int pstride = ((sel & 1u) ? Lx - 1 : 1) * ((sel & 2u) ? Ly - 1 : 1);
         // offsets of the (up to four) cell-tile entries holding this point
-        const int o11 = (d.x & (1u << 13)) ? base : -1;
-        const int o10 = (d.x & (1u << 14)) ? base - TILE + P : -1;
-        const int o01 = (d.x & (1u << 15)) ? base - bcx * TILE + P * RS : -1;
-        const int o00 = (d.x & (1u << 16)) ? base - (bcx + 1) * TILE + P * RS + P : -1;
+        const int o11 = (d.x & (1u << 14)) ? base : -1;
+        const int o10 = (d.x & (1u << 15)) ? base - TILE + P : -1;
+        const int o01 = (d.x & (1u << 16)) ? base - bcx * TILE + P * RS : -1;
+        const int o00 = (d.x & (1u << 17)) ? base - (bcx + 1) * TILE + P * RS + P : -1;
 #pragma unroll
         for (int k = 0; k <= P; ++k) {
           T sum = 0;
