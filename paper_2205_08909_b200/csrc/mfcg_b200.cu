@@ -236,7 +236,8 @@ static int op_create_impl(mfcg_ctx* ctx, const mfcg_op_desc* d, mfcg_op* op) {
     g.B[k] = std::min(b, g.cells[k]);
   }
   {
-    int bz = d->brick[2] > 0 ? d->brick[2] : std::min(16, g.cells[2]);
+    // default depth: 16 cell layers, 32 for p <= 3 (thin layers: +3 % measured, profiles/r01_notes.md)
+    int bz = d->brick[2] > 0 ? d->brick[2] : std::min(p <= 3 ? 32 : 16, g.cells[2]);
     bz = std::min(bz, g.cells[2]);
     if (d->brick[2] <= 0) {
       auto count = [&](int z) {
