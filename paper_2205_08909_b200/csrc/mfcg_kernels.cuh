@@ -33,6 +33,12 @@
 #define MFCG_CHECK(...)
 #endif
 
+// experiment: ring depth MFCG_STAGES for the separable kernel of degree MFCG_STAGES_P
+#ifndef MFCG_STAGES
+#define MFCG_STAGES 2
+#define MFCG_STAGES_P 0
+#endif
+
 namespace mfcg {
 
 typedef long long i64;
@@ -194,9 +200,12 @@ template <int P, int G = 0> struct Geo {
   static constexpr int NTILE = G ? 3 : 2;               // scratch tiles per cell
   static constexpr int WX = (P * Cfg<P, G>::BX + 1) | 1; // window row stride, odd
   static constexpr int PLANE = WX * (P * Cfg<P, G>::BY + 1);
-  static constexpr int RB = 2 * P + 1;                  // lattice planes in the ring: two layers share one
+  // layers in flight between the memory and the math warps (ring depth); 2 everywhere, a build
+  // parameter for experiments on the degrees whose shared memory allows more
+  static constexpr int NS = (G == 0 && P == MFCG_STAGES_P) ? MFCG_STAGES : 2;
+  static constexpr int RB = NS * P + 1;                 // lattice planes in the ring: consecutive layers share one
   static constexpr int NRING = Cfg<P, G>::ONCHIP ? 3 : 1;  // p' (+ r', 1/diag)
-  static constexpr int HEADER = 320;                    // 27 entity starts, 6 mbarriers
+  static constexpr int HEADER = 320;                    // 27 entity starts, 3 * NS mbarriers
   template <typename T> __host__ __device__ static constexpr size_t red_offset() {
     return (HEADER + sizeof(T) * (size_t)(NRING * RB * PLANE + PLANE + NTILE * NCELL * TILE) + 15) & ~(size_t)15;
   }
@@ -548,7 +557,8 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
         const SolveState* __restrict__ st, double* __restrict__ partials, int brick_offset) {
   constexpr int N = P + 1, RS = Geo<P, G>::RS, PSTR = Geo<P, G>::PSTR, TILE = Geo<P, G>::TILE, WX = Geo<P, G>::WX,
                 PLANE = Geo<P, G>::PLANE, NCELL = Geo<P, G>::NCELL, RB = Geo<P, G>::RB,
-                NT_C = Cfg<P, G>::NT_C, NT_P = Cfg<P, G>::NT_P, KC = Cfg<P, G>::KC, HE = EOShape<N>::HE;
+                NT_C = Cfg<P, G>::NT_C, NT_P = Cfg<P, G>::NT_P, KC = Cfg<P, G>::KC, HE = EOShape<N>::HE,
+                NS = Geo<P, G>::NS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   i64* st27 = reinterpret_cast<i64*>(smem_raw);                               // 27 entity starts
   // full[2] (memory -> math), ringfree[2] (ring planes of a layer read), vdone[2] (v of a layer stored)
@@ -592,12 +602,11 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
     st27[tid] = g.ent_start[((i64)(2 * mz + ez) * (2 * g.mb[1] + 1) + (2 * my + ey)) * (2 * g.mb[0] + 1) + 2 * mx + ex];
   }
   if (tid == 32) {
-    mbar_init(&bars[0], NT_P);
-    mbar_init(&bars[1], NT_P);
-    mbar_init(&bars[2], NT_C);
-    mbar_init(&bars[3], NT_C);
-    mbar_init(&bars[4], NT_C);
-    mbar_init(&bars[5], NT_C);
+    for (int sidx = 0; sidx < NS; ++sidx) {
+      mbar_init(&bars[sidx], NT_P);            // full
+      mbar_init(&bars[NS + sidx], NT_C);       // ring free
+      mbar_init(&bars[2 * NS + sidx], NT_C);   // v stored
+    }
   }
   for (int i = tid; i < PLANE; i += NT_C + NT_P) carry[i] = (T)0;
   if (MODE == 1 && G == 0 && tab.diag_onfly)
@@ -724,11 +733,11 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
     if (!PER_BRICK_SUMS && !ONCHIP && (ptid & 31) == 0)
       for (int q = 0; q < 7; ++q) red[pwarp * 7 + q] = 0.0;
     MFCG_TIC(tp);
-    for (int L = 0; L < bcz + 2; ++L) {
-      const int stage = L & 1;
+    for (int L = 0; L < bcz + NS; ++L) {  // the post of a layer runs NS iterations after its fill
+      const int stage = L % NS;
       if (PF > 0) prefetch_layer(L + PF);
-      // the ring planes layer L overwrites were last read by the x sweep of layer L-2
-      if (L >= 2 && L < bcz) role_wait<NT_P>(&bars[2 + stage], ((L >> 1) - 1) & 1, pwarp == 0, 2);
+      // the ring planes layer L overwrites were last read by the x sweep of layer L-NS
+      if (L >= NS && L < bcz) role_wait<NT_P>(&bars[NS + stage], ((L / NS) - 1) & 1, pwarp == 0, 2);
       MFCG_TOC(tp, 0);
       if (L < bcz) {
         // ---- fill the ring with the planes layer L adds (plane 0 is shared with layer L-1)
@@ -864,11 +873,11 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
         mbar_arrive(&bars[stage]);  // layer L full
         MFCG_TOC(tp, 1);
       }
-      if (MODE == 1 && !ONCHIP && L >= 2 && !(MFCG_SKIP & 4)) {
-        role_wait<NT_P>(&bars[4 + stage], ((L >> 1) - 1) & 1, pwarp == 0, 2);  // v of layer L-2 stored
+      if (MODE == 1 && !ONCHIP && L >= NS && !(MFCG_SKIP & 4)) {
+        role_wait<NT_P>(&bars[2 * NS + stage], ((L / NS) - 1) & 1, pwarp == 0, 2);  // v of layer L-NS stored
         // ---- post sums of layer L-2 (solvers.py:692-698): its v is final and, like r, p and
         // 1/diag, still resident in L2; one contiguous run per vector
-        const int Lp = L - 2;
+        const int Lp = L - NS;
         const int Klo = Lp == 0 ? 1 : Lp * P, Khi = Lp * P + P - 1;
         const int nitem = nint2d > 0 ? (Khi - Klo + 1) * nint2d : 0;
         const i64 gbase = st_int + (i64)nint2d * (Klo - 1);
@@ -935,14 +944,14 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
       for (int qq = 0; qq < 7; ++qq) red[(tid >> 5) * 7 + qq] = 0.0;
     MFCG_TIC(tc);
     for (int L = 0; L < bcz; ++L) {
-      const int stage = L & 1;
+      const int stage = L % NS;
       const int s0 = (L * P) % RB;
 #ifndef MFCG_LEADER_POLL
       if (L > 0) math_barrier<NT_C>();        // every math thread is done with the previous gather's tiles
-      mbar_wait(&bars[stage], (L >> 1) & 1);  // layer L full
+      mbar_wait(&bars[stage], (L / NS) & 1);  // layer L full
 #else
       // layer L full; the barrier also says every math thread is done with the previous gather's tiles
-      if (tid < 32) mbar_wait(&bars[stage], (L >> 1) & 1);
+      if (tid < 32) mbar_wait(&bars[stage], (L / NS) & 1);
       math_barrier<NT_C>();
 #endif
       MFCG_TOC(tc, 4);
@@ -1001,7 +1010,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             for (int i = 0; i < N; ++i) At[k * PSTR + j * RS + i] = out[i];
           }
         }
-        if (!ONCHIP) mbar_arrive(&bars[2 + stage]);  // this thread has read its ring rows of layer L
+        if (!ONCHIP) mbar_arrive(&bars[NS + stage]);  // this thread has read its ring rows of layer L
         math_barrier<NT_C>();
         sweep(1, 0, false, false, At, 0, At);
         math_barrier<NT_C>();
@@ -1146,7 +1155,7 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
             for (int i = 0; i < N; ++i) bo[i] = out[i];
           }
         }
-        if (!ONCHIP) mbar_arrive(&bars[2 + stage]);  // this thread has read its ring rows of layer L
+        if (!ONCHIP) mbar_arrive(&bars[NS + stage]);  // this thread has read its ring rows of layer L
         MFCG_TOC(tc, 5);
         math_barrier<NT_C>();
         MFCG_TOC(tc, 8);
@@ -1293,8 +1302,8 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
 #pragma unroll
           for (int qq = 0; qq < 7; ++qq) red[(tid >> 5) * 7 + qq] += s[qq];
       }
-      if (ONCHIP) mbar_arrive(&bars[2 + stage]);  // the on-chip post reads the ring in the gather
-      mbar_arrive(&bars[4 + stage]);  // v of layer L stored (orders the v stores before the post loads)
+      if (ONCHIP) mbar_arrive(&bars[NS + stage]);  // the on-chip post reads the ring in the gather
+      mbar_arrive(&bars[2 * NS + stage]);  // v of layer L stored (orders the v stores before the post loads)
       MFCG_TOC(tc, 9);
     }
   }
