@@ -8,9 +8,12 @@ every call raises.  The library is built in-tree by
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libmfcg_b200.so"
+# MFCG_LIB: explicit path of a variant build (timing experiments, -DMFCG_BOUNDS); the production
+# library is never overwritten by experiments
+LIB_PATH = Path(os.environ.get("MFCG_LIB") or Path(__file__).resolve().parent / "libmfcg_b200.so")
 
 OK, EINVAL, ENOMEM, ECUDA, EBREAKDOWN, EUNSUPPORTED = range(6)
 

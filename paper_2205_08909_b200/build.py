@@ -36,7 +36,7 @@ def _nvcc() -> str:
 
 def _sources():
     return [CSRC / "mfcg_b200.cu", CSRC / "mfcg_inst.cu", CSRC / "mfcg_kernels.cuh",
-            CSRC / "mfcg_engine.cuh", INCLUDE / "mfcg_b200.h"]
+            CSRC / "mfcg_engine.cuh", CSRC / "mfcg_brick2.cuh", INCLUDE / "mfcg_b200.h"]
 
 
 def is_stale() -> bool:
@@ -48,15 +48,36 @@ def is_stale() -> bool:
 
 def _compile(args):
     src, obj, extra = args
-    cmd = [_nvcc(), *NVCC_FLAGS, *os.environ.get("MFCG_EXTRA_FLAGS", "").split(), *extra, "-c", str(src), "-o", str(obj)]
+    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-c", str(src), "-o", str(obj)]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
         raise RuntimeError(f"nvcc failed: {' '.join(cmd)}\n{proc.stdout}\n{proc.stderr}")
     return obj
 
 
+def build_variant(out: Path, flags, degrees=DEGREES, verbose: bool = False) -> Path:
+    """A variant build (extra -D flags) into its own file and object directory; load it with MFCG_LIB=<out>."""
+    out = Path(out)
+    objdir = OBJ / ("var_" + out.stem)
+    objdir.mkdir(parents=True, exist_ok=True)
+    jobs = [(CSRC / "mfcg_b200.cu", objdir / "mfcg_b200.o", list(flags))]
+    jobs += [(CSRC / "mfcg_inst.cu", objdir / f"mfcg_inst_p{p}.o",
+              [f"-DMFCG_P={p}", *flags] if p in degrees else [f"-DMFCG_P={p}", "-DMFCG_STUB"]) for p in DEGREES]
+    with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as pool:
+        objs = list(pool.map(_compile, jobs))
+    cmd = [_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", str(out), *map(str, objs)]
+    proc = subprocess.run(cmd, capture_output=True, text=True)
+    if proc.returncode != 0:
+        raise RuntimeError(f"link failed: {' '.join(cmd)}\n{proc.stdout}\n{proc.stderr}")
+    if verbose:
+        print(f"built {out}", file=sys.stderr)
+    return out
+
+
 def build_library(force: bool = False, verbose: bool = False) -> Path:
     """Compile and link the shared library if it is missing or out of date."""
+    if os.environ.get("MFCG_EXTRA_FLAGS"):
+        raise RuntimeError("MFCG_EXTRA_FLAGS would change the production library: use build_variant() + MFCG_LIB")
     if not force and not is_stale():
         return LIB
     OBJ.mkdir(parents=True, exist_ok=True)
@@ -75,4 +96,11 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
 
 
 if __name__ == "__main__":
-    build_library(force="--force" in sys.argv, verbose=True)
+    if "--variant" in sys.argv:  # python -m paper_2205_08909_b200.build --variant tools/varlibs/x.so -DMFCG_TIMING ...
+        i = sys.argv.index("--variant")
+        flags = [a for a in sys.argv[i + 2:] if not a.startswith("--degrees=")]
+        degs = [a for a in sys.argv[i + 2:] if a.startswith("--degrees=")]
+        degrees = tuple(int(x) for x in degs[0].split("=")[1].split(",")) if degs else DEGREES
+        build_variant(Path(sys.argv[i + 1]), flags, degrees=degrees, verbose=True)
+    else:
+        build_library(force="--force" in sys.argv, verbose=True)

@@ -4,12 +4,14 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "mfcg_b200.h"
 #include "mfcg_kernels.cuh"
+#include "mfcg_brick2.cuh"
 
 namespace mfcg {
 
@@ -177,6 +179,15 @@ class Engine : public EngineBase {
       smem_ = (int)Geo<P, 0>::template smem_bytes<T>();
       MFCG_CUDA(cudaFuncSetAttribute(k_brick<P, T, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
       MFCG_CUDA(cudaFuncSetAttribute(k_brick<P, T, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
+      if constexpr (Brick2Enabled<P>::value) {
+        // the persistent TMA-fed kernel of the merged iteration (mfcg_brick2.cuh); MFCG_BRICK2=0 keeps the
+        // first-generation kernel for comparisons
+        const char* env = std::getenv("MFCG_BRICK2");
+        brick2_ok_ = !(env && env[0] == '0');
+        if (brick2_ok_)
+          MFCG_CUDA(cudaFuncSetAttribute(k_brick2<P, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)Geo2<P, T>::SMEM));
+      }
     }
     vgrid_ = c_->ctx->sm_count * 8;
     // one scalar field per component, fields 256-byte aligned; the gaps stay zero
@@ -199,6 +210,8 @@ class Engine : public EngineBase {
     for (int d = 0; d < 3; ++d) out->brick[d] = c_->grid.B[d];
     out->threads = general_ ? Cfg<P, 1>::THREADS : Cfg<P, 0>::THREADS;
     out->smem_bytes = smem_;
+    if constexpr (Brick2Enabled<P>::value)
+      if (brick2_ok_) { out->threads = Geo2<P, T>::THREADS; out->smem_bytes = (int)Geo2<P, T>::SMEM; }
     out->geometry_bytes = geo_bytes_;
   }
 
@@ -377,7 +390,13 @@ class Engine : public EngineBase {
         if (mode == 0)
           k_brick<P, T, 0, 0><<<nb, Cfg<P, 0>::THREADS, smem_, stream()>>>(
               c_->grid, tab_, gen_, geo_, s_, nullptr, vv_, nullptr, nullptr, nullptr, nullptr, nullptr, off);
-        else
+        else if (use_brick2_) {
+          if constexpr (Brick2Enabled<P>::value) {
+            const unsigned grid2 = std::min<unsigned>(nb, (unsigned)c_->ctx->sm_count);
+            k_brick2<P, T><<<grid2, Geo2<P, T>::THREADS, Geo2<P, T>::SMEM, stream()>>>(
+                c_->grid, tab_, tab_.diag_onfly ? 1 : 2, pv_, vv_, rr_, xx_, c_->d_state, part_, off, (int)nb);
+          }
+        } else
           k_brick<P, T, 1, 0><<<nb, Cfg<P, 0>::THREADS, smem_, stream()>>>(
               c_->grid, tab_, gen_, geo_, nullptr, pv_, vv_, rr_, xx_, mm_, c_->d_state, part_, off);
       } else if (c_->geometry != MFCG_GEOM_QUADRATIC_COMPUTE) {
@@ -601,6 +620,7 @@ class Engine : public EngineBase {
     if ((rc = load_vec(a->b, a->location, r_))) return rc;
     const bool prec = a->variant == MFCG_COMBINED_PCG;
     tab_.diag_onfly = (prec && !a->inv_diag && !general_) ? 1 : 0;
+    use_brick2_ = brick2_ok_ && (tab_.diag_onfly || !prec);
     if (prec) {
       if (a->inv_diag) {
         if ((rc = load_vec(a->inv_diag, a->location, minv_))) return rc;
@@ -774,6 +794,7 @@ class Engine : public EngineBase {
   void* geo_b_ = nullptr;
   i64 geo_bytes_ = 0;
   bool general_ = false;
+  bool brick2_ok_ = false, use_brick2_ = false;
   void* plane_[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [side lo/hi][send/recv]
   double* d_sums_ = nullptr;
   double* diag_raw_ = nullptr;  // slab runs: diagonal before the interface exchange
@@ -919,6 +940,8 @@ int Engine<P, T>::solve(const mfcg_solve_args* a, mfcg_solve_result* res) {
   if ((rc = load_vec(a->b, a->location, merged ? r_ : v_))) return rc;
   // the operator's own Jacobi diagonal on an affine mesh is separable: interior DoFs compute it
   tab_.diag_onfly = (merged && prec && !a->inv_diag && !general_ && a->fused) ? 1 : 0;
+  // persistent kernel: 1/diag is either the operator's own (computed in the kernel) or the identity
+  use_brick2_ = brick2_ok_ && merged && a->fused && (tab_.diag_onfly || !prec);
   if (prec) {
     if (a->inv_diag) {
       if ((rc = load_vec(a->inv_diag, a->location, minv_, 1))) return rc;
@@ -996,10 +1019,15 @@ int Engine<P, T>::solve(const mfcg_solve_args* a, mfcg_solve_result* res) {
   {
     unsigned long long h[16];
     cudaMemcpyFromSymbol(h, g_phase_cycles, sizeof(h));
+#if 1
+    const char* names[16] = {"S.wait_lfull", "S.compute", "S.wait_tiles", "S.store", "M.wait_tiles", "M.zsweep", "M.gather", "M.barrier",
+                             "P.wait_tupd", "P.wait_ldone", "P.issue", "", "U.wait_ldone", "U.wait_tfull", "U.update", "U.perim+tail"};
+#else
     const char* names[16] = {"P.wait_empty", "P.fill", "P.post", "", "C.wait_full", "C.x", "C.y", "C.z", "C.bar", "C.gather",
                              "", "", "", "", "", ""};
+#endif
     std::fprintf(stderr, "[mfcg timing] cycles of one warp per role summed over blocks and launches (op launches %lld):\n", (long long)op_launches_);
-    for (int i = 0; i < 10; ++i)
+    for (int i = 0; i < 16; ++i)
       if (names[i][0]) std::fprintf(stderr, "  %-14s %14llu\n", names[i], h[i]);
     unsigned long long z[16] = {0};
     cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));

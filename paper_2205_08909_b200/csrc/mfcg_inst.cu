@@ -11,6 +11,14 @@ namespace mfcg {
 #define MFCG_CAT2(a, b) a##b
 #define MFCG_CAT(a, b) MFCG_CAT2(a, b)
 
+#ifdef MFCG_STUB
+// variant builds for timing experiments carry one degree only (tools/varlibs, build.build_variant)
+EngineBase* MFCG_CAT(make_engine_p, MFCG_P)(OpCommon*, int* status) {
+  set_error("this variant build does not contain the degree");
+  *status = MFCG_EUNSUPPORTED;
+  return nullptr;
+}
+#else
 EngineBase* MFCG_CAT(make_engine_p, MFCG_P)(OpCommon* c, int* status) {
   if (c->precision == 0) {
     auto* e = new Engine<MFCG_P, double>(c);
@@ -21,5 +29,6 @@ EngineBase* MFCG_CAT(make_engine_p, MFCG_P)(OpCommon* c, int* status) {
   if ((*status = e->init()) != MFCG_OK) { delete e; return nullptr; }
   return e;
 }
+#endif
 
 }  // namespace mfcg
