@@ -4,6 +4,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <new>
 
 #include "mfcg_engine.cuh"
@@ -244,7 +245,23 @@ static int op_create_impl(mfcg_ctx* ctx, const mfcg_op_desc* d, mfcg_op* op) {
         return (i64)((g.cells[0] + g.B[0] - 1) / g.B[0]) * ((g.cells[1] + g.B[1] - 1) / g.B[1]) *
                ((g.cells[2] + z - 1) / z);
       };
-      while (bz > 1 && count(bz) < 4 * (i64)ctx->c.sm_count) bz = (bz + 1) / 2;
+      const char* env = std::getenv("MFCG_BRICK2");
+      const bool persistent = d->geometry == MFCG_GEOM_AFFINE && p >= 2 && p <= 5 && !(env && env[0] == '0');
+      if (persistent) {
+        // merged iterations run in the persistent kernel (mfcg_brick2.cuh): block i walks bricks i, i + SMs, ...
+        // Pick the depth that minimises the layers of the busiest block, with ~0.7 layer per brick for the
+        // restart of the pipeline; deeper bricks also have fewer shared DoFs (measured at 116^3 Q5:
+        // depth 16 / 29 / 58 -> 2.65 / 2.58 / 2.66 ms per launch, profiles/r02_notes.md)
+        const int lo = std::min(4, g.cells[2]), hi = std::min(64, g.cells[2]);
+        double best = 1e300;
+        for (int z = lo; z <= hi; ++z) {
+          const i64 per_block = (count(z) + ctx->c.sm_count - 1) / ctx->c.sm_count;
+          const double cost = (double)per_block * (z + 0.7);
+          if (cost < best - 1e-9) { best = cost; bz = z; }
+        }
+      } else {
+        while (bz > 1 && count(bz) < 4 * (i64)ctx->c.sm_count) bz = (bz + 1) / 2;
+      }
     }
     g.B[2] = bz;
   }

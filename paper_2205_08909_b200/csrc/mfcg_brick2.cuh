@@ -65,7 +65,13 @@ template <int ID, int COUNT> __device__ __forceinline__ void named_arrive() {
                         // stores, 4 no update at all, 8 no gather, 16 no z sweep, 32 no plane sweeps
 #endif
 #ifndef MFCG_B2_NT
-#define MFCG_B2_NT 4   // transient plane slots (p, v, x)
+#define MFCG_B2_NT 5   // transient plane slots (p, v, x)
+#endif
+#ifndef MFCG_B2_RLAYERS
+#define MFCG_B2_RLAYERS 2  // layers of lattice planes in the ring: the update runs RLAYERS - 1 layers ahead of the gather
+#endif
+#ifndef MFCG_B2_UNR
+#define MFCG_B2_UNR 2
 #endif
 #ifndef MFCG_B2_NRL
 #define MFCG_B2_NRL 3  // layers of r' staged on chip
@@ -92,13 +98,13 @@ template <int P, typename T> struct Geo2 {
   static constexpr int FP_MAX = (P * BX + 1) * (P * BY + 1);
   // ring of lattice planes: three consecutive layers, also across brick boundaries (3 x (P+1) planes): the
   // update warps may run two layers ahead of the gather
-  static constexpr int RB = 3 * P + 3;
+  static constexpr int RLAYERS = MFCG_B2_RLAYERS, RB = RLAYERS * (P + 1);
   static constexpr int PER16 = 16 / (int)sizeof(T);
   static constexpr int NT = MFCG_B2_NT, NRL = MFCG_B2_NRL;
-  // warpgroups: 0 = plane sweeps in registers (3 warps, NS1) + the producer warp, 1-2 = z sweep + gather (NLM),
-  // 3 = update warps (NUPD)
+  // 16 warps: 0-2 plane sweeps in registers (NS1), 3 producer, 4-11 z sweep + gather (NLM), 12-15 update (NUPD).
+  // (7 + 5 warps for gather / update measured 5 % slower at 116^3, profiles/r02_notes.md)
   static constexpr int NS1 = 96, NLM = 256, NUPD = 128, THREADS = 512;
-  static constexpr int REG_S1 = 232, REG_LIGHT = 88, REG_UPD = 104;  // setmaxnreg: 128 * (232 + 2 * 88 + 104) == 512 * 128
+  static constexpr int REG_S1 = 232, REG_LIGHT = 88, REG_UPD = 104;  // setmaxnreg per warpgroup: 128 * (232 + 2 * 88 + 104) == 512 * 128
   // Rows of cell row cy are shifted by SK * cy so that the 16 (fp64) / 32 (fp32) lanes of a shared-memory
   // wavefront -- the same plane entry of consecutive cells -- fall into different banks.
   static constexpr int bank_conflicts(int sk) {
@@ -148,8 +154,9 @@ struct Hdr2 {
   i64 st27[3][28];                       // 27 entity starts of the current brick, one copy per role
   unsigned long long tfull[8], tupd[8];  // transient slot loaded / updated
   unsigned long long lfull[4], ldone[4]; // layer ready for the math warps / gather of a layer finished
-  double lsum[4][4][2];                  // r.r and r.Mr of a layer, per update warp
+  double lsum[4][8][2];                  // r.r and r.Mr of a layer, per update warp
   double bsum[2];                        // their running sums over the brick
+  int sdone[8];                          // last plane consumed from a transient slot
   double red[8][8];
 };
 static_assert(sizeof(Hdr2) <= 2048, "header");
@@ -164,6 +171,7 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
                 PLANE = G2::PLANE, NCELL = G2::NCELL, RB = G2::RB, PER16 = G2::PER16, PLB = G2::PLB,
                 NT = G2::NT, NRL = G2::NRL, NS1 = G2::NS1, NLM = G2::NLM, NUPD = G2::NUPD, HE = EOShape<N>::HE,
                 NTHR = G2::THREADS, T_PROD = NS1, T_LM = 128, T_UPD = 128 + NLM;
+  static_assert(T_UPD + NUPD == NTHR && T_UPD % 128 == 0, "thread map: roles with different register budgets fill whole warpgroups");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Hdr2& H = *reinterpret_cast<Hdr2*>(smem_raw);
   T* const ring = reinterpret_cast<T*>(smem_raw + G2::OFF_RING);
@@ -183,7 +191,7 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
   const int xmode = st->xmode;
 
   if (tid == 0) {
-    for (int i = 0; i < NT; ++i) { mbar_init(&H.tfull[i], 1); mbar_init(&H.tupd[i], 32); }
+    for (int i = 0; i < NT; ++i) { mbar_init(&H.tfull[i], 1); mbar_init(&H.tupd[i], 32); H.sdone[i] = -1; }
     for (int i = 0; i < 4; ++i) mbar_init(&H.lfull[i], NUPD);
     for (int i = 0; i < 4; ++i) mbar_init(&H.ldone[i], NLM);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -269,9 +277,11 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
     const int nplanes = nint2d > 0 ? Lz - 1 : 0;
     const int fw = Lx + 1, fp = fw * (Ly + 1);
     if (bcx != cur_bcx || bcy != cur_bcy) {  // every role is between two bricks here
-      __syncthreads();
+      // non-aligned barrier: the roles arrive from different code, possibly with diverged warps (the aligned
+      // bar.sync of __syncthreads() hung here within a few hundred launches on ragged brick grids)
+      named_barrier<5, NTHR>();
       build_tables(bcx, bcy);
-      __syncthreads();
+      named_barrier<5, NTHR>();
       cur_bcx = bcx;
       cur_bcy = bcy;
     }
@@ -288,6 +298,9 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
           const int q = q_base + K - 1, slot = q % NT;
           B2_TIC(tp);
           if (q >= NT) mbar_wait(&H.tupd[slot], ((q - NT) / NT) & 1);  // the slot's previous plane has been read
+#ifdef MFCG_B2_EXP_AHEAD
+          if (q >= MFCG_B2_EXP_AHEAD) mbar_wait(&H.tupd[(q - MFCG_B2_EXP_AHEAD) % NT], ((q - MFCG_B2_EXP_AHEAD) / NT) & 1);
+#endif
           B2_TOC(tp, 0);
           const int gf = g_base + K / P;  // layer whose gather finishes the plane
           if ((K % P == 0 || K == 1) && gf >= NRL) mbar_wait(&H.ldone[(gf - NRL) & 3], ((gf - NRL) >> 2) & 1);
@@ -333,7 +346,7 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
         const int gl = g_base + L;
         B2_TIC(tu);
         // the ring planes this layer overwrites were last read by the gather three layers back
-        if (gl >= 3) mbar_wait(&H.ldone[(gl - 3) & 3], ((gl - 3) >> 2) & 1);
+        if (gl >= G2::RLAYERS) mbar_wait(&H.ldone[(gl - G2::RLAYERS) & 3], ((gl - G2::RLAYERS) >> 2) & 1);
         B2_TOC(tu, 0);
                 // (b) brick-boundary points of the layer's planes (pre-updated by k_pre): issue the loads now,
         //     consume them after the interior planes
@@ -365,7 +378,11 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
         if (nint2d > 0)
           for (int K = Kfirst; K <= Klast; ++K) {
             const int q = q_base + K - 1, slot = q % NT;
+#ifdef MFCG_B2_EXP_SYNC
+            if (q % (NUPD / 32) == uw) {
+#else
             if (q % (NUPD / 32) != uw) continue;  // whole planes round-robin over the update warps
+#endif
             const int gf = g_base + K / P;
             T* Rb = Rbuf + ((gf % NRL) * P + K % P) * PLB;
             const T* Pb = Tbuf + (slot * 3 + 0) * PLB;
@@ -380,6 +397,15 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
             if (tail0 < head) tail0 = head;
             const T* dcls = dtab + (K % P) * P * P;
             T* rplane = ring + ((kb_base + K) % RB) * PLANE;
+            // Phase parity only tells "this phase" from "the previous one", and this warp's previous plane sat
+            // in another slot: the slot's previous plane (another warp's) may not even have landed yet, and the
+            // parity of the phase before that would let the wait below through (seen as wrong results / hangs
+            // once in a few hundred launches on ragged brick grids with NT = 5).  The warp that consumed the
+            // slot's previous plane publishes its number; once that is visible the barrier is in our phase.
+            if (q >= NT) {
+              const volatile int* sd = H.sdone + slot;
+              while (*sd < q - NT) {}
+            }
             mbar_wait(&H.tfull[slot], (q / NT) & 1);
             B2_TOC(tu, 1);
             // 16-byte granules of the staged plane (buffer index bi = off + e).  Granules [g_lo, g_hi) lie
@@ -407,7 +433,7 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
               Vec* Pg = reinterpret_cast<Vec*>(Pv + (e0 - off));
               Vec* Xg = reinterpret_cast<Vec*>(X + (e0 - off));
               const unsigned short* it0 = itab - off;
-              constexpr int UNR = XM ? 1 : 2;
+              constexpr int UNR = XM ? 1 : MFCG_B2_UNR;
 #pragma unroll 1
               for (int g0 = g_lo + lane; g0 < g_hi; g0 += UNR * 32) {
                 Vec rr[UNR], vv[UNR], pq[UNR], xx[UNR];
@@ -460,9 +486,16 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
             else if (xmode == 0) update_plane(std::integral_constant<int, 0>());
             else if (xmode == 1) update_plane(std::integral_constant<int, 1>());
             else update_plane(std::integral_constant<int, 2>());
+            if (lane == 0) *(volatile int*)(H.sdone + slot) = q;
             mbar_arrive(&H.tupd[slot]);  // the transient slot (p, v, x) has been read
+#ifdef MFCG_B2_EXP_SYNC
+            }
+            named_barrier<2, NUPD>();
+            {
+#endif
             B2_TOC(tu, 2);
           }
+        B2_TOC(tu, 5);
         asm volatile("cp.async.wait_all;" ::: "memory");
 #pragma unroll
         for (int kk = 0; kk < P + 1; ++kk) {
@@ -489,6 +522,7 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
           for (int it = ut; it < nint2d; it += NUPD, ++cnt)
             if (fbits & (1u << cnt)) pl[itab[it] & 1023u] = (T)0;
         }
+        B2_TOC(tu, 4);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           ls0 += __shfl_xor_sync(0xffffffffu, ls0, o);
@@ -496,7 +530,7 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
         }
         if ((ut & 31) == 0) { H.lsum[gl & 3][uw][0] = ls0; H.lsum[gl & 3][uw][1] = ls4; }
         mbar_arrive(&H.lfull[gl & 3]);
-        B2_TOC(tu, 3);
+        B2_TOC(tu, 5);
       }
     } else if constexpr (ROLE == 0) {
       // ================================ plane sweeps (warpgroup 0) ================================
@@ -741,7 +775,8 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
   }
 #ifdef MFCG_TIMING
   if (tid == 0 || tid == T_LM || tid == T_PROD || tid == T_UPD)
-    for (int i = 0; i < 4; ++i) atomicAdd(&g_phase_cycles[(tid == 0 ? 0 : (tid == T_LM ? 4 : (tid == T_PROD ? 8 : 12))) + i], tacc[i]);
+    for (int i = 0; i < (tid == T_UPD ? 6 : 4); ++i)
+      atomicAdd(&g_phase_cycles[(tid == 0 ? 0 : (tid == T_LM ? 4 : (tid == T_PROD ? 8 : 12))) + i], tacc[i]);
 #endif
   };
   // register re-allocation between the warpgroups: the plane sweeps hold 2 (p+1)^2 values per thread

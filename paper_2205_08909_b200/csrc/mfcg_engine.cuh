@@ -1017,19 +1017,19 @@ int Engine<P, T>::solve(const mfcg_solve_args* a, mfcg_solve_result* res) {
   }
 #ifdef MFCG_TIMING
   {
-    unsigned long long h[16];
+    unsigned long long h[24];
     cudaMemcpyFromSymbol(h, g_phase_cycles, sizeof(h));
 #if 1
-    const char* names[16] = {"S.wait_lfull", "S.compute", "S.wait_tiles", "S.store", "M.wait_tiles", "M.zsweep", "M.gather", "M.barrier",
-                             "P.wait_tupd", "P.wait_ldone", "P.issue", "", "U.wait_ldone", "U.wait_tfull", "U.update", "U.perim+tail"};
+    const char* names[24] = {"S.wait_lfull", "S.compute", "S.wait_tiles", "S.store", "M.wait_tiles", "M.zsweep", "M.gather", "M.barrier",
+                             "P.wait_tupd", "P.wait_ldone", "P.issue", "", "U.wait_ldone", "U.wait_tfull", "U.update", "U.perim_issue", "U.tail", "U.reduce+arrive", "", "", "", "", "", ""};
 #else
     const char* names[16] = {"P.wait_empty", "P.fill", "P.post", "", "C.wait_full", "C.x", "C.y", "C.z", "C.bar", "C.gather",
                              "", "", "", "", "", ""};
 #endif
     std::fprintf(stderr, "[mfcg timing] cycles of one warp per role summed over blocks and launches (op launches %lld):\n", (long long)op_launches_);
-    for (int i = 0; i < 16; ++i)
+    for (int i = 0; i < 24; ++i)
       if (names[i][0]) std::fprintf(stderr, "  %-14s %14llu\n", names[i], h[i]);
-    unsigned long long z[16] = {0};
+    unsigned long long z[24] = {0};
     cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
   }
 #endif

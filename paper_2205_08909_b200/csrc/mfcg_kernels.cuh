@@ -46,7 +46,7 @@ typedef long long i64;
 #ifdef MFCG_TIMING
 // Light phase timing: one designated warp per role accumulates clock deltas in shared
 // memory (single writer per slot) and flushes them once at kernel end.
-static __device__ unsigned long long g_phase_cycles[16];
+static __device__ unsigned long long g_phase_cycles[24];
 #define MFCG_TIC(var) long long var = clock64()
 #define MFCG_TOC(var, slot)                                                                     \
   do {                                                                                          \
@@ -1362,20 +1362,33 @@ __global__ void k_pre(BrickGrid g, i64 lo, i64 hi, int init_v, T* __restrict__ R
   if (!st->active) return;
   const T am1 = (T)st->am1, bm1 = (T)st->bm1, xc1 = (T)st->xc1, xc2 = (T)st->xc2;
   const int xmode = st->xmode;
-  for (i64 i = lo + blockIdx.x * (i64)blockDim.x + threadIdx.x; i < hi; i += (i64)gridDim.x * blockDim.x) {
-    T r = R[i], p = Pv[i];
-    const T v = V[i], m = Minv[i];
-    if (xmode) {
-      T x = X[i];
-      if (xmode == 2) x += xc1 * p + xc2 * (p - m * r);
-      else x += xc1 * p;
-      X[i] = x;
+  constexpr int U = 4;  // independent loads in flight per thread
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 i0 = lo + blockIdx.x * (i64)blockDim.x + threadIdx.x; i0 < hi; i0 += U * stride) {
+    T r[U], p[U], v[U], m[U], x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const i64 i = i0 + u * stride;
+      if (i < hi) {
+        r[u] = R[i]; p[u] = Pv[i]; v[u] = V[i]; m[u] = Minv[i];
+        if (xmode) x[u] = X[i];
+      }
     }
-    r -= am1 * v;
-    p = m * r + bm1 * p;
-    R[i] = r;
-    Pv[i] = p;
-    if (init_v) V[i] = (T)0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const i64 i = i0 + u * stride;
+      if (i >= hi) break;
+      if (xmode) {
+        if (xmode == 2) x[u] += xc1 * p[u] + xc2 * (p[u] - m[u] * r[u]);
+        else x[u] += xc1 * p[u];
+        X[i] = x[u];
+      }
+      r[u] -= am1 * v[u];
+      p[u] = m[u] * r[u] + bm1 * p[u];
+      R[i] = r[u];
+      Pv[i] = p[u];
+      if (init_v) V[i] = (T)0;
+    }
   }
 }
 
@@ -1387,18 +1400,36 @@ __global__ void k_post(BrickGrid g, i64 lo, i64 hi, int fix_constrained, const T
   __shared__ double red[7 * 32];
   if (!st->active) return;
   double s[7] = {0, 0, 0, 0, 0, 0, 0};
-  for (i64 i = lo + blockIdx.x * (i64)blockDim.x + threadIdx.x; i < hi; i += (i64)gridDim.x * blockDim.x) {
-    const double r = (double)R[i], p = (double)Pv[i], m = (double)Minv[i];
-    double v = (double)V[i];
-    unsigned char flag = i >= g.n_int ? g.mask[i - g.n_int] : (unsigned char)0;
-    if (fix_constrained && (flag & 1)) {  // identity row: v_c = p_c
-      v = p;
-      V[i] = (T)p;
+  constexpr int U = 4;  // independent loads in flight per thread
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 i0 = lo + blockIdx.x * (i64)blockDim.x + threadIdx.x; i0 < hi; i0 += U * stride) {
+    T rr[U], pp[U], mm[U], vv[U];
+    unsigned char ff[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const i64 i = i0 + u * stride;
+      ff[u] = 0;
+      if (i < hi) {
+        rr[u] = R[i]; pp[u] = Pv[i]; mm[u] = Minv[i]; vv[u] = V[i];
+        if (i >= g.n_int) ff[u] = g.mask[i - g.n_int];
+      }
     }
-    if (flag & 2) continue;  // ghost copy of the lower slab's plane: counted there
-    const double mr = m * r, mv = m * v;
-    s[0] += r * r; s[1] += p * v; s[2] += r * v; s[3] += v * v;
-    s[4] += r * mr; s[5] += r * mv; s[6] += v * mv;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const i64 i = i0 + u * stride;
+      if (i >= hi) break;
+      const double r = (double)rr[u], p = (double)pp[u], m = (double)mm[u];
+      double v = (double)vv[u];
+      const unsigned char flag = ff[u];
+      if (fix_constrained && (flag & 1)) {  // identity row: v_c = p_c
+        v = p;
+        V[i] = (T)p;
+      }
+      if (flag & 2) continue;  // ghost copy of the lower slab's plane: counted there
+      const double mr = m * r, mv = m * v;
+      s[0] += r * r; s[1] += p * v; s[2] += r * v; s[3] += v * v;
+      s[4] += r * mr; s[5] += r * mv; s[6] += v * mv;
+    }
   }
   block_reduce7_store(s, red, partials + (i64)blockIdx.x * 8);
 }

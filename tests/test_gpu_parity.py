@@ -369,3 +369,36 @@ def test_full_size_properties(n):
     assert rel(op.apply(2.0 * mer.x - 3.0 * b), 2.0 * Ax - 3.0 * Ab) < 1e-12
     # energy checksum: x.b == x.A x up to the residual (symmetric positive operator)
     assert abs(mer.x @ Ax - mer.x @ b) <= 2 * mer.residual * bn * np.linalg.norm(mer.x)
+
+
+def test_repeated_solves_on_ragged_brick_grid():
+    """The persistent kernel walks several bricks per block and pipelines across brick boundaries; on a
+    49 x 49 x 20 mesh (845 bricks of 4 x 4 x 4 cells with 1-cell-wide ragged bricks, 5-6 bricks per block)
+    every block changes brick shape several times per launch.  A mis-ordered hand-over between the roles
+    shows up as a history that differs between identical solves (it did: NT = 5 transient slots with four
+    update warps let a warp wait two barrier phases ahead, once in a few hundred launches), so: the
+    first solve against the oracle, and 40 repeated 200-iteration solves against the first."""
+    S = _solvers()
+    p = 5
+    m, h, plan = host_tables((49, 49, 20), p)
+    op = gpu_operator(m, h, plan, p, p + 1, brick=(0, 0, 4))
+    assert op.info()["n_bricks"] == 845
+    b = seeded_rhs(h)
+    minv = op.compute_diagonal()
+    prob = oracle_problem(m, h, p, p + 1)
+    first = S.solve("combined_pcg", op, b, minv=minv, config=S.SolverConfig(fixed_iterations=12))
+    import mfcg_oracle_c as oc
+    if oc.available():
+        cp = oc.CProblem(prob)
+        _, _, hist = cp.combined_pcg(b, minv.inverse_diagonal, 12)   # hist[k] = alpha, beta, gamma, residual
+        assert rel(hist_array(first.history)[:, 3], hist[:, 3]) < 1e-10
+    ref = None
+    worst = 0.0
+    for _ in range(40):
+        res = S.solve("combined_pcg", op, b, minv=minv, config=S.SolverConfig(fixed_iterations=200))
+        H = hist_array(res.history)[:, 3]
+        if ref is None:
+            ref = H
+        worst = max(worst, float(np.max(np.abs(H - ref) / ref)))
+    print(f"repeated ragged solves: max relative history deviation {worst:.2e}")
+    assert worst < 1e-9   # run-to-run differences come from the order of the RED.F64 adds only

@@ -5,5 +5,5 @@
 for lib in tools/varlibs/*.so; do
   MFCG_LIB=$PWD/$lib timeout 100 python bench.py --cells 73 73 73 --iters 20 --steps 2 --warmup 1 --no-cpu-baseline 2>gpurun_out/$(basename $lib).err | python -c "
 import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print('$lib', 'kernel_ms %.3f it_ms %.3f'%(r['kernel_ms'], r['iteration_ms']))"
-  grep -A16 'mfcg timing' gpurun_out/$(basename $lib).err | tail -16 | awk '{printf "%s %.0f | ", $1, $2/2960/200} END {print ""}'
+  grep -A18 'mfcg timing' gpurun_out/$(basename $lib).err | tail -18 | awk '{printf "%s %.0f | ", $1, $2/2960/200} END {print ""}'
 done
