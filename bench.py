@@ -11,9 +11,14 @@ the JSON line.  `value` times K solves with b and x resident in HBM; `e2e` times
 the same K solves through the public API `solve("combined_pcg", op, b_host, ...)`
 with pinned host buffers (H2D of b and D2H of x inside the timed region).
 
+N > 1: one process per GPU (torchrun; `--gpus N` without torchrun re-launches itself
+under it), z-slabs of BASELINE configs[4]: `--scaling weak` (default) 80^3 cells per
+GPU, `--scaling strong` 160^3 cells in total.
+
 `--impl reference` times the CPU implementation of the same path (the oracle
 port of the pure-Python reference; `oracle/_ref` cannot exist because the
-reference has no compiled sources) on the host cores on a bounded sample.
+reference has no compiled sources) on the host cores on a bounded sample of the
+SAME mesh: a few merged-PCG iterations instead of the full count.
 """
 import argparse
 import json
@@ -133,7 +138,7 @@ class CpuPort:
         self.b = seeded_rhs(h)
         self.prob = orc.Problem(tuple(cells), mesh.extents, 0.0, p, p + 1, h.cell_index_blocks,
                                 h.constrained_dofs, h.n_dofs)
-        self.minv = orc.inverse_diagonal(self.prob)
+        self.minv = orc.inverse_diagonal_affine(self.prob)  # closed form, pinned to inverse_diagonal in tests
         self.cp = None
         self.cores = 1
         self.note = "NumPy restatement (oracle/mfcg_oracle.py)"
@@ -158,22 +163,30 @@ class CpuPort:
 
 
 def run_reference(args, rank):
+    """The reference arm: the CPU port of the reference's merged Jacobi-PCG on the host cores, on the
+    SAME mesh as the GPU arm (BASELINE configs[1] top rung at N = 1), for `--ref-iters` iterations per
+    step instead of the GPU arm's `--iters` (DoF*it/s does not depend on the iteration count)."""
     if rank != 0:
         return
-    n = args.ref_cells
-    port = CpuPort((n, n, n), args.degree)
+    cells = tuple(args.ref_cells_xyz) if args.ref_cells_xyz else workload_cells(args, 1)
+    t0 = time.perf_counter()
+    port = CpuPort(cells, args.degree)
+    setup = time.perf_counter() - t0
     times = [port.seconds(args.ref_iters) for _ in range(args.warmup + args.steps)][args.warmup:]
     total = sum(times)
     value = port.n_dofs * args.ref_iters * len(times) / total
-    sample = (f"{n}^3 cells Q{args.degree} ({port.n_dofs} DoFs), {args.ref_iters} merged-PCG iterations per step "
-              f"of the same seeded problem (the reference itself is sequential NumPy and cannot run the "
-              f"full workload); {port.note}")
+    sample = (f"{cells[0]}x{cells[1]}x{cells[2]} cells Q{args.degree} ({port.n_dofs} DoFs), {args.ref_iters} merged-PCG "
+              f"iterations per step of the same seeded problem; {port.note}; {port.cores} threads; "
+              f"setup {setup:.0f} s (not timed)")
+    cfg = workload_config(args, 1, cells=cells, iters=args.ref_iters)
+    cfg["bounded_sample"] = (f"{args.ref_iters} iterations per step instead of {args.iters}: same mesh, same "
+                             f"operator, same right-hand side")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (uniform[-1,1] RHS, seed 0)",
-        "config": workload_config(args, args.gpus),
+        "config": cfg,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": port.cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -186,19 +199,27 @@ def workload_cells(args, n_gpus):
         return tuple(args.cells)
     if n_gpus == 1:
         return (116, 116, 116)
+    if args.scaling == "strong":
+        return (160, 160, 160)
     return (80, 80, 80 * n_gpus)
 
 
-def workload_config(args, n_gpus):
-    cells = workload_cells(args, n_gpus)
+def workload_config(args, n_gpus, cells=None, iters=None):
+    cells = tuple(cells) if cells else workload_cells(args, n_gpus)
+    iters = iters or args.iters
     n_dofs = int(np.prod([c * args.degree + 1 for c in cells])) * args.components
-    which = ("BASELINE configs[1] top rung" if n_gpus == 1 and not args.cells
-             else ("BASELINE configs[4] weak scaling, 80^3 cells per GPU in z-slabs" if not args.cells
-                   else "custom"))
+    if args.cells:
+        which = "custom"
+    elif n_gpus == 1:
+        which = "BASELINE configs[1] top rung"
+    elif args.scaling == "strong":
+        which = "BASELINE configs[4] strong scaling, 160^3 cells in z-slabs"
+    else:
+        which = "BASELINE configs[4] weak scaling, 80^3 cells per GPU in z-slabs"
     return {"workload": f"Q{args.degree} {'Poisson' if args.components == 1 else '3-component Laplace (BP4 type)'}, Cartesian {cells[0]}x{cells[1]}x{cells[2]} cells, "
-                        f"{n_dofs} DoFs, fp64, Jacobi, seeded uniform[-1,1] RHS, {args.iters} merged-CG "
+                        f"{n_dofs} DoFs, fp64, Jacobi, seeded uniform[-1,1] RHS, {iters} merged-CG "
                         f"iterations per step ({which})",
-            "cells": list(cells), "degree": args.degree, "n_dofs": n_dofs, "iterations_per_step": args.iters,
+            "cells": list(cells), "degree": args.degree, "n_dofs": n_dofs, "iterations_per_step": iters,
             "variant": args.variant, "geometry": args.geometry, "deformation": args.deform, "l2": "inputs larger than L2 (each vector >> 126 MB); no flush needed",
             "parallelism": "1 GPU" if n_gpus == 1 else f"z-slabs x{n_gpus}"}
 
@@ -238,7 +259,8 @@ def run_slabs(args, rank, local_rank, world):
     vals = rng.uniform(-1.0, 1.0, (nzg * p + 1) * plane)
     b = vals[slab.global_nodes - z0 * p * plane]
     b[slab.handler.constrained_dofs] = 0.0
-    b_dev = torch.from_numpy(b).cuda()
+    b_host = torch.from_numpy(b).pin_memory()
+    b_dev = b_host.cuda()
     x_dev = torch.empty_like(b_dev)
     cfg = SolverConfig(fixed_iterations=args.iters)
     lib_stream = torch.cuda.ExternalStream(_lib.stream_handle(local_rank))
@@ -266,6 +288,19 @@ def run_slabs(args, rank, local_rank, world):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total = float(t.item())
     clocks = sampler.stop()
+    # end to end through SlabGroup.solve with HOST buffers: every step copies the rank's part of b from pinned
+    # host memory and x back (inside the library call); wall clock between barriers, max over ranks
+    group.solve(args.variant, [b_host.numpy()], cfg)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        group.solve(args.variant, [b_host.numpy()], cfg)
+    torch.cuda.synchronize()
+    dist.barrier()
+    te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    t_e2e = float(te.item())
     if rank == 0:
         value = n_global * args.iters * args.steps / (ms_total * 1e-3)
         peak, peak_src = measured_peak()
@@ -273,7 +308,7 @@ def run_slabs(args, rank, local_rank, world):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
             "data": "synthetic (uniform[-1,1] RHS, seed 0, constrained entries zeroed)",
             "config": workload_config(args, world),
             "roofline": {"bound": "hbm", "kernel": "whole merged iteration, all GPUs",
@@ -281,9 +316,11 @@ def run_slabs(args, rank, local_rank, world):
                          "frac": value * BYTES_PER_DOF_IT / 1e9 / (peak * world), "peak_source": peak_src,
                          "traffic": None},
             "cpu_baseline": None,
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-                    "note": "per-rank slabs stay device resident in the multi-GPU run; the host round trip is "
-                            "measured at N=1"},
+            "e2e": {"value": n_global * args.iters * args.steps / t_e2e, "unit": UNIT,
+                    "h2d_bytes_per_step": 8 * n_local * world, "d2h_bytes_per_step": 8 * n_local * world,
+                    "ms_per_step": 1e3 * t_e2e / args.steps,
+                    "timer": "host wall clock between barriers around K SlabGroup.solve calls with pinned host "
+                             "buffers, max over ranks"},
             "gpu_launches": int(launches), "clocks": clocks,
             "extra": {"final_relative_residual": res.residual, "dofs_per_gpu": n_local,
                       "plane_bytes_per_exchange": 8 * plane, "bricks_per_gpu": info["n_bricks"],
@@ -310,8 +347,14 @@ def main():
     ap.add_argument("--deform", type=float, default=0.0)
     ap.add_argument("--components", type=int, default=1, choices=[1, 3],
                     help="3: vector Laplacian of the BP4 type (SURVEY.md 8f row 3); single GPU only")
-    ap.add_argument("--ref-cells", type=int, default=32)
-    ap.add_argument("--ref-iters", type=int, default=60)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = 80^3 cells per GPU, strong = 160^3 cells in total (BASELINE configs[4])")
+    ap.add_argument("--ref-cells-xyz", type=int, nargs=3, default=None,
+                    help="reference arm / cpu_baseline mesh (default: the GPU arm's mesh)")
+    ap.add_argument("--ref-iters", type=int, default=2,
+                    help="merged-PCG iterations per step of the CPU port (bounded sample of the same workload)")
+    ap.add_argument("--cpu-baseline-cells", type=int, default=48,
+                    help="edge of the cube the cpu_baseline leg of the GPU arm times (bounded sample)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
@@ -325,6 +368,20 @@ def main():
     import torch
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a B200: the hot path has no CPU fallback")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` without torchrun: re-launch under it, one rank per GPU
+        if torch.cuda.device_count() < args.gpus:
+            raise SystemExit(f"--gpus {args.gpus} but only {torch.cuda.device_count()} GPU(s) are visible")
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator / transport lines on stderr
+        os.execvp(sys.executable, [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                                   f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+                                   "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]])
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} does not match WORLD_SIZE {world}")
     torch.cuda.set_device(local_rank)
     if world > 1:
         run_slabs(args, rank, local_rank, world)
@@ -389,7 +446,8 @@ def main():
     achieved = kernel_bytes / (op_ms * 1e-3) / 1e9
     it_ms = rt.device_stats["solve_ms"] / args.iters
     roofline = {
-        "bound": "hbm", "kernel": f"k_brick<{p},{'double' if w == 8 else 'float'},merged>",
+        "bound": "hbm", "kernel": (f"k_brick2<{p},{'double' if w == 8 else 'float'}> (persistent, cp.async.bulk fed)" if info["threads"] == 512
+                                   else f"k_brick<{p},{'double' if w == 8 else 'float'},merged>"),
         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
         "traffic": None, "algorithmic_bytes_per_launch": kernel_bytes, "kernel_ms": op_ms,
         "iteration_ms": it_ms, "kernel_share_of_step": op_ms / it_ms,
@@ -404,7 +462,8 @@ def main():
             tj = json.loads(prof.read_text())
             if args.geometry == "affine" and args.degree == 5 and args.precision == "fp64" and nc == 1:
                 roofline["traffic"] = tj["bytes_per_dof"] * n
-                roofline["traffic_source"] = "profiles/traffic.json: " + tj["source"] + f"; {tj['workload']}, scaled by n_dofs"
+                roofline["traffic_source"] = ("from_profile (not measured in this run): profiles/traffic.json, " + tj["source"]
+                                              + f"; {tj['workload']}, bytes per DoF scaled by n_dofs")
         except Exception:
             pass
 
@@ -425,12 +484,14 @@ def main():
 
     cpu = None
     if not args.no_cpu_baseline:
-        nref = args.ref_cells
+        nref = args.cpu_baseline_cells
         port = CpuPort((nref, nref, nref), p)
-        secs = port.seconds(args.ref_iters)
-        cpu = {"value": port.n_dofs * args.ref_iters / secs, "unit": UNIT, "cores": port.cores, "kind": "port",
-               "sample": f"{nref}^3 cells Q{p} ({port.n_dofs} DoFs), {args.ref_iters} merged-PCG "
-                         f"iterations in {secs:.1f} s; {port.note}"}
+        its = max(args.ref_iters, 20)
+        secs = port.seconds(its)
+        cpu = {"value": port.n_dofs * its / secs, "unit": UNIT, "cores": port.cores, "kind": "port",
+               "sample": f"{nref}^3 cells Q{p} ({port.n_dofs} DoFs), {its} merged-PCG iterations in {secs:.1f} s "
+                         f"(bounded sample of the same problem family; `--impl reference` times the full mesh); "
+                         f"{port.note}"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,

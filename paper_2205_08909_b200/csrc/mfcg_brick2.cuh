@@ -73,6 +73,9 @@ template <int ID, int COUNT> __device__ __forceinline__ void named_arrive() {
 #ifndef MFCG_B2_UNR
 #define MFCG_B2_UNR 2
 #endif
+#ifndef MFCG_B2_UNRX
+#define MFCG_B2_UNRX 1
+#endif
 #ifndef MFCG_B2_NRL
 #define MFCG_B2_NRL 3  // layers of r' staged on chip
 #endif
@@ -342,6 +345,7 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
         const unsigned sel = d.y >> 22;
         ppstride = ((sel & 1u) ? Lx - 1 : 1) * ((sel & 2u) ? Ly - 1 : 1);
       }
+      double ls0 = 0.0, ls4 = 0.0;  // r.r and r.Mr of this thread over the brick
       for (int L = 0; L < bcz; ++L) {
         const int gl = g_base + L;
         B2_TIC(tu);
@@ -374,7 +378,6 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
         // (a) interior planes: pre update in place in the staged planes (solvers.py:660-690)
         const int Kfirst = L == 0 ? 1 : L * P + 1;
         const int Klast = L * P + P < Lz - 1 ? L * P + P : Lz - 1;
-        double ls0 = 0.0, ls4 = 0.0;
         if (nint2d > 0)
           for (int K = Kfirst; K <= Klast; ++K) {
             const int q = q_base + K - 1, slot = q % NT;
@@ -433,7 +436,7 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
               Vec* Pg = reinterpret_cast<Vec*>(Pv + (e0 - off));
               Vec* Xg = reinterpret_cast<Vec*>(X + (e0 - off));
               const unsigned short* it0 = itab - off;
-              constexpr int UNR = XM ? 1 : MFCG_B2_UNR;
+              constexpr int UNR = XM ? MFCG_B2_UNRX : MFCG_B2_UNR;
 #pragma unroll 1
               for (int g0 = g_lo + lane; g0 < g_hi; g0 += UNR * 32) {
                 Vec rr[UNR], vv[UNR], pq[UNR], xx[UNR];
@@ -523,12 +526,14 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
             if (fbits & (1u << cnt)) pl[itab[it] & 1023u] = (T)0;
         }
         B2_TOC(tu, 4);
+        if (L == bcz - 1) {  // handed over with the brick's last layer
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          ls0 += __shfl_xor_sync(0xffffffffu, ls0, o);
-          ls4 += __shfl_xor_sync(0xffffffffu, ls4, o);
+          for (int o = 16; o > 0; o >>= 1) {
+            ls0 += __shfl_xor_sync(0xffffffffu, ls0, o);
+            ls4 += __shfl_xor_sync(0xffffffffu, ls4, o);
+          }
+          if ((ut & 31) == 0) { H.lsum[gl & 3][uw][0] = ls0; H.lsum[gl & 3][uw][1] = ls4; }
         }
-        if ((ut & 31) == 0) { H.lsum[gl & 3][uw][0] = ls0; H.lsum[gl & 3][uw][1] = ls4; }
         mbar_arrive(&H.lfull[gl & 3]);
         B2_TOC(tu, 5);
       }
@@ -632,8 +637,8 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
         { volatile double* vv_ = &H.bsum[0]; (void)*vv_; }  // the barrier blocks at the first dependent access
 #endif
         B2_TOC(tm, 0);
-        if (lt == 0) {
-          double a0_ = H.bsum[0], a4_ = H.bsum[1];
+        if (lt == 0 && L == bcz - 1) {  // r.r and r.Mr of the brick from the update warps
+          double a0_ = 0.0, a4_ = 0.0;
           for (int w = 0; w < NUPD / 32; ++w) { a0_ += H.lsum[gl & 3][w][0]; a4_ += H.lsum[gl & 3][w][1]; }
           H.bsum[0] = a0_; H.bsum[1] = a4_;
         }

@@ -26,6 +26,24 @@ void set_error(const std::string& msg);
     }                                                                                       \
   } while (0)
 
+// Owners for objects created inside entry points that have early error returns.
+struct EventPair {
+  cudaEvent_t a = nullptr, b = nullptr;
+  ~EventPair() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+  cudaError_t create() {
+    cudaError_t e = cudaEventCreate(&a);
+    return e != cudaSuccess ? e : cudaEventCreate(&b);
+  }
+};
+template <typename T> struct DevBuf {
+  T* p = nullptr;
+  ~DevBuf() { if (p) cudaFree(p); }
+  cudaError_t alloc(size_t n) { return cudaMalloc(&p, sizeof(T) * (n ? n : 1)); }
+};
+
 struct Ctx {
   int device = 0;
   int sm_count = 148;
@@ -856,7 +874,7 @@ int Engine<P, T>::run_merged(const mfcg_solve_args* a, int limit) {
       launches_ += 2 * C_ + 1;
     }
     MFCG_CUDA(cudaGetLastError());
-    if (!fixed && (it % 16 == 0)) {
+    if (!fixed && (it % 8 == 0)) {
       MFCG_CUDA(cudaMemcpyAsync(c_->h_state, c_->d_state, sizeof(SolveState), cudaMemcpyDeviceToHost, stream()));
       MFCG_CUDA(cudaStreamSynchronize(stream()));
       if (!c_->h_state->active) break;
@@ -897,7 +915,7 @@ int Engine<P, T>::run_standard(const mfcg_solve_args* a, int limit, bool prec) {
     k_std_update_p<T><<<vgrid_, VT, 0, stream()>>>(n, p_, z, c_->d_state);
     launches_ += 2;
     MFCG_CUDA(cudaGetLastError());
-    if (!fixed && (it % 16 == 0)) {
+    if (!fixed && (it % 8 == 0)) {
       MFCG_CUDA(cudaMemcpyAsync(c_->h_state, c_->d_state, sizeof(SolveState), cudaMemcpyDeviceToHost, stream()));
       MFCG_CUDA(cudaStreamSynchronize(stream()));
       if (!c_->h_state->active) break;
@@ -931,9 +949,9 @@ int Engine<P, T>::solve(const mfcg_solve_args* a, mfcg_solve_result* res) {
   time_kernels_ = a->time_kernels != 0;
   event_cursor_ = 0;
 
-  cudaEvent_t t0, t1;
-  MFCG_CUDA(cudaEventCreate(&t0));
-  MFCG_CUDA(cudaEventCreate(&t1));
+  EventPair ev;  // destroyed on every return path
+  MFCG_CUDA(ev.create());
+  cudaEvent_t t0 = ev.a, t1 = ev.b;
   MFCG_CUDA(cudaEventRecord(t0, stream()));
 
   // right-hand side: merged variants start with r = b, the standard ones stage b in v
@@ -971,8 +989,6 @@ int Engine<P, T>::solve(const mfcg_solve_args* a, mfcg_solve_result* res) {
     if ((rc = store_vec(x_, a->x, a->location))) return rc;
     MFCG_CUDA(cudaStreamSynchronize(stream()));
     res->converged = 1;
-    cudaEventDestroy(t0);
-    cudaEventDestroy(t1);
     return MFCG_OK;
   }
   SolveState s0;
@@ -1003,8 +1019,6 @@ int Engine<P, T>::solve(const mfcg_solve_args* a, mfcg_solve_result* res) {
   const SolveState& s = *c_->h_state;
   float ms = 0.f;
   MFCG_CUDA(cudaEventElapsedTime(&ms, t0, t1));
-  cudaEventDestroy(t0);
-  cudaEventDestroy(t1);
   res->solve_ms = ms;
   if (time_kernels_) {
     double acc = 0.0;
@@ -1036,7 +1050,9 @@ int Engine<P, T>::solve(const mfcg_solve_args* a, mfcg_solve_result* res) {
   res->kernel_launches = launches_;
   res->operator_launches = op_launches_;
   res->iterations = s.k;
-  res->matvecs = (int)op_launches_;
+  // solvers.py:218, 705: one operator application per iteration; launches enqueued behind the converged
+  // iteration (the host polls the device state every 8 iterations in tolerance mode) return at once
+  res->matvecs = s.k;
   res->residual = s.residual;
   res->breakdown = s.breakdown;
   res->breakdown_iteration = s.breakdown_iteration;

@@ -80,19 +80,26 @@ def test_config1_solves_vs_reference(golden):
             H, R = hist_array(res.history), g[f"{variant}_hist"]
             assert res.iterations == 100 and res.matvecs == 100 and H.shape == R.shape
             dev = np.abs(H[:, 3] - R[:, 3]) / R[:, 3]
+            xdev = rel(res.x, g[f"{variant}_x"])
             if variant in ("pcg", "combined_pcg"):
                 E = g[f"{variant}_hist_reordered"]
                 env = np.maximum.accumulate(np.abs(E[:, 3] - R[:, 3]) / R[:, 3])
                 strict = env < 1e-11
                 assert dev[strict].max() < 1e-10, (variant, fused, dev[strict].max())
                 # beyond that point CG amplifies rounding noise exponentially and the GPU's
-                # atomic accumulation order changes from run to run: stay within two orders
-                # of magnitude of the reference's own re-ordering envelope
-                assert np.all(dev[~strict] <= 100 * env[~strict] + 1e-10), (variant, fused)
+                # atomic accumulation order changes from run to run: stay within one order
+                # of magnitude of the reference's own re-ordering envelope (SURVEY.md 8c iii)
+                ratio = float(np.max(dev[~strict] / (env[~strict] + 1e-11)))
+                print(f"config1 {variant} fused={fused}: strict zone {int(strict.sum())} its, max dev there "
+                      f"{dev[strict].max():.2e}; beyond: max dev/envelope {ratio:.2f}; |x - x_ref|/|x_ref| {xdev:.2e}")
+                assert np.all(dev[~strict] <= 10 * env[~strict] + 1e-10), (variant, fused, ratio)
+            else:
+                print(f"config1 {variant}: max residual dev over 100 its {dev.max():.2e}; x dev {xdev:.2e}")
             assert dev[:40].max() < 1e-10
             for col in range(3):
                 assert rel(H[:40, col], R[:40, col]) < 1e-10, (variant, fused, col)
-            assert rel(res.x, g[f"{variant}_x"]) < 1e-7
+            # observed on B200: 6e-11 .. 2e-9 (the reference against a re-ordered copy of itself: 6e-11 .. 3e-9)
+            assert xdev < 1e-8, (variant, fused, xdev)
             # true residual of the returned iterate agrees with the recurred one
             true_res = np.linalg.norm(b - op.apply(res.x)) / np.linalg.norm(b)
             assert abs(true_res - res.residual) < 1e-9
@@ -112,6 +119,7 @@ def test_tolerance_termination_and_edge_cases(golden):
         res = S.solve(variant, op, g["b"], minv=minv, config=S.SolverConfig(tolerance=1e-6, max_iterations=500))
         assert [res.iterations, int(res.converged)] == list(g[f"{variant}_tol_iters"])
         assert len(res.history) == res.iterations
+        assert res.matvecs == res.iterations   # solvers.py:218, 705 (launches behind the converged iteration are no-ops)
         assert rel(hist_array(res.history)[:, 3], g[f"{variant}_tol_hist"][:, 3]) < 1e-8
     zero = S.solve("combined_pcg", op, np.zeros(h.n_dofs), minv=minv)
     assert zero.iterations == 0 and zero.converged and not zero.history and np.all(zero.x == 0)

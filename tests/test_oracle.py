@@ -69,6 +69,8 @@ def test_apply_and_diagonal_match_reference(golden, ci):
     assert rel(orc.apply(prob, u), g[f"c{ci}_Au"]) < 1e-12
     if con:
         assert rel(orc.inverse_diagonal(prob), g[f"c{ci}_invdiag"]) < 1e-12
+        # the closed form used for the full-size CPU baseline (bench.py) against the same reference fixture
+        assert rel(orc.inverse_diagonal_affine(prob), g[f"c{ci}_invdiag"]) < 1e-12
         # constrained rows copy through bit-exactly (reference tests/test_operator.py:126-131)
         assert np.array_equal(orc.apply(prob, u)[h.constrained_dofs], u[h.constrained_dofs])
 

@@ -165,3 +165,38 @@ def test_nccl_binding_single_rank():
     grp = slabs.SlabGroup([op]).solve("combined_pcg", [b], cfg)[0]
     assert rel(hist_array(grp.history), hist_array(one.history)) < 1e-12
     assert rel(grp.x, one.x) < 1e-12
+
+
+@pytest.mark.gpu
+def test_nccl_send_recv_to_self_through_group_exchange(monkeypatch):
+    """ncclSend / ncclRecv, their dtype constant and the stream ordering of `group_exchange`, on one GPU: a
+    middle slab (neighbours below and above) on a one-rank communicator with both peers redirected to the
+    rank itself (MFCG_NCCL_SELF_PEER=1; send-to-self inside one NCCL group is legal).  Sends and receives to
+    the same peer match in posting order, so the slab receives its own bottom / top plane contributions and
+    adds them once more: v doubles on the two interface planes and is untouched elsewhere, compared with the
+    same slab as a stand-alone operator (no neighbours, same constraint set)."""
+    import torch  # noqa: F401  (loads libnccl.so.2 into the process)
+    from paper_2205_08909_b200.operator import MatrixFreeOperator, OperatorSpec
+    monkeypatch.setenv("MFCG_NCCL_SELF_PEER", "1")
+    slabs.init_comm(0, slabs.new_unique_id(), 0, 1)
+    p, cells = 3, (5, 4, 12)
+    gm = pmesh.build_cartesian_mesh(cells)
+    s = slabs.build_slab(gm, p, 4, 4)           # cell layers 4..7 of 12: neighbours on both sides
+    assert s.has_lower and s.has_upper
+    plan = dofs.make_batches(s.mesh, dofs.batch_size(p, 1, 8), "morton")
+    spec = OperatorSpec("laplace", 1, p, p + 1, pmesh.GeometryVariant.AFFINE)
+    op_mid = MatrixFreeOperator(spec, s.mesh, s.handler, plan, slab_z0=s.z0, global_cells_z=s.global_cells_z)
+    # the same cells as a mesh of their own: extents scaled so that h is the same, same constraint set
+    alone_mesh = pmesh.build_cartesian_mesh(s.mesh.cells_per_dim, (1.0, 1.0, 4.0 / 12.0))
+    op_alone = MatrixFreeOperator(spec, alone_mesh, s.handler, plan)
+    u = np.random.default_rng(5).standard_normal(s.handler.n_dofs)
+    got = slabs.SlabGroup([op_mid]).apply([u])[0]
+    ref = op_alone.apply(u)
+    lower, upper = slabs.interface_plane_nodes(s, "lower"), slabs.interface_plane_nodes(s, "upper")
+    con = np.zeros(s.handler.n_dofs, bool)
+    con[s.handler.constrained_dofs] = True
+    expect = ref.copy()
+    for plane in (lower, upper):
+        free = plane[~con[plane]]
+        expect[free] = 2.0 * ref[free]          # own contribution received once more from "the neighbour"
+    assert rel(got, expect) < 1e-12
