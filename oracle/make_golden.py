@@ -255,7 +255,64 @@ def locality():
     np.savez_compressed(OUT / "locality.npz", **out)
 
 
+def bp_canonical():
+    """BP3 / BP4 exactly as the reference's harness builds them (bench.py:153-187 defaults: sine-deformed mesh
+    0.05, final_tensor_load, n_q = p + 2): manufactured RHS, one apply, the Jacobi diagonal, 25 iterations of
+    pcg and combined_pcg."""
+    from mfcg.bench import assemble_problem
+    out = {}
+    for key, (bp, p, cells) in {"bp3": ("BP3", 5, (3, 3, 3)), "bp4": ("BP4", 5, (2, 2, 3)),
+                                "bp3_p2": ("BP3", 2, (4, 3, 5))}.items():
+        op, b, minv = assemble_problem(bp, p, cells)
+        assert op.spec.n_q_1d == p + 2 and op.mesh.deformation == 0.05
+        u = np.random.default_rng(17).standard_normal(op.n_dofs)
+        out[f"{key}_b"] = b
+        out[f"{key}_u"] = u
+        out[f"{key}_Au"] = op.apply(u)
+        out[f"{key}_invdiag"] = minv.inverse_diagonal
+        for variant_name in ("pcg", "combined_pcg"):
+            res = solve(variant_name, op, b, minv=minv, config=SolverConfig(fixed_iterations=25))
+            out[f"{key}_{variant_name}_hist"] = hist_array(res)
+            out[f"{key}_{variant_name}_x"] = res.x
+    np.savez_compressed(OUT / "bp_canonical.npz", **out)
+
+
+def big_table_digests():
+    """SHA-256 of the reference's integer tables on meshes too large to commit as arrays (32^3 and 48^3 cells,
+    Q5): block table, renumbering (blocks, permutation, constrained tail), Dirichlet set, range schedule
+    first/last, Morton batches.  The package's vectorised tables must reproduce the digests bit for bit."""
+    import hashlib
+    import json
+
+    def dg(a):
+        a = np.ascontiguousarray(a)
+        return hashlib.sha256(a.tobytes()).hexdigest() + f":{a.dtype}:{a.shape}"
+
+    out = {}
+    for n in (32, 48):
+        mesh = build_cartesian_mesh((n, n, n))
+        h = distribute_dofs(mesh, 5, 1, constrain_boundary=True)
+        plan = make_batches(mesh, batch_size(5, 1, 8), "morton")
+        hr = renumber_optimized(h, plan)
+        sch = compute_range_schedule(hr, plan)
+        out[str(n)] = {
+            "n_dofs": int(h.n_dofs),
+            "blocks": dg(h.cell_index_blocks), "constrained": dg(h.constrained_dofs),
+            "batches": dg(np.concatenate([np.asarray(b) for b in plan.batches])),
+            "ren_blocks": dg(hr.cell_index_blocks), "ren_permutation": dg(hr.permutation),
+            "ren_constrained": dg(hr.constrained_dofs),
+            "schedule_first": dg(sch.first_touch_batch), "schedule_last": dg(sch.last_touch_batch),
+        }
+        print("digests", n, out[str(n)]["n_dofs"], flush=True)
+    (OUT / "big_tables.json").write_text(json.dumps(out, indent=1))
+
+
 if __name__ == "__main__":
+    import sys as _sys
+    if len(_sys.argv) > 1:  # regenerate selected fixtures only: python oracle/make_golden.py bp_canonical ...
+        for name in _sys.argv[1:]:
+            globals()[name]()
+        raise SystemExit(0)
     tables()
     harness_rhs()
     numbering()
@@ -265,5 +322,7 @@ if __name__ == "__main__":
     curved()
     vector3()
     locality()
+    bp_canonical()
+    big_table_digests()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)

@@ -12,6 +12,7 @@
 #include "mfcg_b200.h"
 #include "mfcg_kernels.cuh"
 #include "mfcg_brick2.cuh"
+#include "mfcg_cellpath.cuh"
 
 namespace mfcg {
 
@@ -181,11 +182,20 @@ class Engine : public EngineBase {
     tab_.wa[P] = tab_.da[P] = 0.0;
     tab_.diag_onfly = 0;
     general_ = c_->geometry != MFCG_GEOM_AFFINE;
-    if (general_) {
-      if (c_->nq != N) {
-        set_error("curved geometry variants need n_q_1d == p+1 on the GPU path");
-        return MFCG_EUNSUPPORTED;
-      }
+    // curved mesh with more quadrature points than nodes per direction (BP3 / BP4 of the reference, n_q = p+2):
+    // the cell-by-cell path (mfcg_cellpath.cuh); merged solves then run pre / apply / post as three kernels
+    cellpath_ = general_ && c_->nq != N;
+    if (cellpath_) {
+      for (int q = 0; q < c_->nq; ++q)
+        for (int i = 0; i < N; ++i) { ctab_.S[q * N + i] = c_->S[q * N + i]; ctab_.D[q * N + i] = c_->D[q * N + i]; }
+      ctab_.n = N;
+      ctab_.nq = c_->nq;
+      cell_smem_ = (int)(sizeof(T) * 6 * c_->nq * c_->nq * c_->nq + sizeof(int) * N * N * N);
+      MFCG_CUDA(cudaFuncSetAttribute(k_cell_general<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, cell_smem_));
+      smem_ = cell_smem_;
+      int rc = build_general_tables();
+      if (rc) return rc;
+    } else if (general_) {
       smem_ = (int)Geo<P, 1>::template smem_bytes<T>();
       MFCG_CUDA(cudaFuncSetAttribute(k_brick<P, T, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
       MFCG_CUDA(cudaFuncSetAttribute(k_brick<P, T, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
@@ -263,7 +273,7 @@ class Engine : public EngineBase {
       set_error("the operator holds no stored geometry table of that kind");
       return MFCG_EINVAL;
     }
-    const i64 nq3 = (i64)N * N * N, nc = c_->n_cells;
+    const i64 nq3 = (i64)c_->nq * c_->nq * c_->nq, nc = c_->n_cells;
     const i64 need = kind == 1 ? nc * nq3 * 6 : nc * nq3 * 10;
     if (n_doubles < need) { set_error("output buffer too small"); return MFCG_EINVAL; }
     const i64 na = kind == 1 ? nc * nq3 * 6 : nc * nq3 * 9;
@@ -404,7 +414,11 @@ class Engine : public EngineBase {
       T* vv_ = v + o;
       T *rr_ = r_ ? r_ + o : nullptr, *xx_ = x_ ? x_ + o : nullptr, *mm_ = minv_ ? minv_ + o : nullptr;
       double* part_ = partials ? partials + 8 * comp * rows_pc_ : nullptr;
-      if (!general_) {
+      if (cellpath_) {
+        if (mode != 0) { set_error("internal error: the cell path has no fused iteration"); return MFCG_ECUDA; }
+        const unsigned cgrid = (unsigned)std::min<i64>(c_->n_cells, (i64)c_->ctx->sm_count * 16);
+        k_cell_general<T><<<cgrid, 128, cell_smem_, stream()>>>(c_->grid, ctab_, geo_, qpt_, c_->n_cells, s_, vv_);
+      } else if (!general_) {
         if (mode == 0)
           k_brick<P, T, 0, 0><<<nb, Cfg<P, 0>::THREADS, smem_, stream()>>>(
               c_->grid, tab_, gen_, geo_, s_, nullptr, vv_, nullptr, nullptr, nullptr, nullptr, nullptr, off);
@@ -443,7 +457,9 @@ class Engine : public EngineBase {
   // dst = A src in brick numbering
   int launch_apply(const T* src, T* dst) {
     const bool has_shared = c_->grid.n_dofs > c_->grid.n_int;
-    if (has_shared) {
+    if (cellpath_) {  // every DoF is accumulated atomically
+      MFCG_CUDA(cudaMemsetAsync(dst, 0, sizeof(T) * nt_, stream()));
+    } else if (has_shared) {
       for (int comp = 0; comp < C_; ++comp) k_surface_init<T><<<vgrid_, VT, 0, stream()>>>(c_->grid, dst + comp * cs_);
       MFCG_CUDA(cudaGetLastError());
       launches_ += C_;
@@ -462,6 +478,7 @@ class Engine : public EngineBase {
   // ------------------------------------------------------------------ slab group interface
  public:
   int g_alloc() override {
+    if (cellpath_) { set_error("z-slabs of curved operators with n_q_1d > p+1 are not supported"); return MFCG_EUNSUPPORTED; }
     const i64 nxy = (i64)(c_->grid.cells[0] * P + 1) * (c_->grid.cells[1] * P + 1);
     for (int side = 0; side < 2; ++side)
       for (int rv = 0; rv < 2; ++rv)
@@ -734,7 +751,8 @@ class Engine : public EngineBase {
   // halves of S and of the collocation derivative Dc, and the device geometry tables
   int build_general_tables() {
     constexpr int H = EOShape<N>::H, HE = EOShape<N>::HE;
-    const std::vector<double>& S = c_->S;  // [q][i], n_q == N
+    const std::vector<double>& S = c_->S;  // [q][i]
+    if (!cellpath_) {  // even/odd halves of S and Dc for the brick kernels (n_q == N)
     // Dc[q][r]: derivative at x_q of the Lagrange polynomial through the quadrature points
     std::vector<double> Dc(N * N, 0.0);
     const std::vector<double>& x = c_->xq;
@@ -766,12 +784,15 @@ class Engine : public EngineBase {
       }
     for (int q = 0; q < HE; ++q)
       for (int r = 0; r < H; ++r) gen_.Bo[q * H + r] = (T)(0.5 * (Dc[q * N + r] - Dc[q * N + (N - 1 - r)]));
-    const PointTab pt = point_table(c_->xq, c_->wq);
-    for (int i = 0; i < N; ++i) {
-      for (int c = 0; c < 3; ++c) { gen_.qv[3 * i + c] = (T)pt.qv[3 * i + c]; gen_.qd[3 * i + c] = (T)pt.qd[3 * i + c]; }
-      gen_.w3[i] = (T)c_->wq[i];
     }
-    const i64 nc = c_->n_cells, nq3 = (i64)N * N * N;
+    const PointTab pt = point_table(c_->xq, c_->wq);
+    if (!cellpath_)
+      for (int i = 0; i < N; ++i) {
+        for (int c = 0; c < 3; ++c) { gen_.qv[3 * i + c] = (T)pt.qv[3 * i + c]; gen_.qd[3 * i + c] = (T)pt.qd[3 * i + c]; }
+        gen_.w3[i] = (T)c_->wq[i];
+      }
+    qpt_ = pt;
+    const i64 nc = c_->n_cells, nq3 = (i64)c_->nq * c_->nq * c_->nq;
     const int kind = c_->geometry;
     double* nodes = nullptr;
     MFCG_CUDA(cudaMemsetAsync(c_->d_flag, 0, sizeof(int), stream()));
@@ -812,6 +833,10 @@ class Engine : public EngineBase {
   void* geo_b_ = nullptr;
   i64 geo_bytes_ = 0;
   bool general_ = false;
+  bool cellpath_ = false;  // curved mesh with n_q_1d != p+1: cell-by-cell apply
+  CellTables ctab_{};
+  PointTab qpt_{};
+  int cell_smem_ = 0;
   bool brick2_ok_ = false, use_brick2_ = false;
   void* plane_[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [side lo/hi][send/recv]
   double* d_sums_ = nullptr;
@@ -836,8 +861,9 @@ int Engine<P, T>::run_merged(const mfcg_solve_args* a, int limit) {
   const bool fixed = a->fixed_iterations >= 0;
   // rows of partial sums: per component, one per brick and one per k_post block (unused rows stay zero)
   const int rows_fused = (int)(rows_pc_ * C_);
+  const bool fused = a->fused && !cellpath_;
   for (int it = 1; it <= limit; ++it) {
-    if (a->fused) {
+    if (fused) {
       if (n_sh > 0) {
         for (int c = 0; c < C_; ++c) {
           const i64 o = c * cs_;
@@ -957,7 +983,7 @@ int Engine<P, T>::solve(const mfcg_solve_args* a, mfcg_solve_result* res) {
   // right-hand side: merged variants start with r = b, the standard ones stage b in v
   if ((rc = load_vec(a->b, a->location, merged ? r_ : v_))) return rc;
   // the operator's own Jacobi diagonal on an affine mesh is separable: interior DoFs compute it
-  tab_.diag_onfly = (merged && prec && !a->inv_diag && !general_ && a->fused) ? 1 : 0;
+  tab_.diag_onfly = (merged && prec && !a->inv_diag && !general_ && a->fused) ? 1 : 0;  // general_ covers the cell path
   // persistent kernel: 1/diag is either the operator's own (computed in the kernel) or the identity
   use_brick2_ = brick2_ok_ && merged && a->fused && (tab_.diag_onfly || !prec);
   if (prec) {

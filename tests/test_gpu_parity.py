@@ -198,6 +198,31 @@ def test_fp32_variant():
 
 
 @pytest.mark.parametrize("p", range(1, 9))
+def test_fp32_all_degrees(p):
+    """BASELINE configs[3]: every degree in fp32 (vectors and operator), 1e-4 relative against the fp64 oracle:
+    one apply, the 20-iteration merged-PCG residual history and the iterate."""
+    S = _solvers()
+    cells = {1: (19, 18, 5), 2: (11, 12, 4), 3: (7, 8, 3), 4: (6, 5, 3), 5: (5, 4, 3), 6: (4, 3, 3),
+             7: (3, 3, 3), 8: (3, 2, 3)}[p]
+    m, h, plan = host_tables(cells, p)
+    prob = oracle_problem(m, h, p, p + 1)
+    op = gpu_operator(m, h, plan, p, p + 1, precision="fp32")
+    u = np.random.default_rng(40 + p).standard_normal(h.n_dofs)
+    assert rel(op.apply(u), orc.apply(prob, u)) < 1e-5
+    minv = orc.inverse_diagonal(prob)
+    b = seeded_rhs(h)
+    for variant, fn in (("combined_pcg", orc.combined_pcg), ("pcg", orc.pcg)):
+        x, k, r, conv, hist = fn(lambda v: orc.apply(prob, v), b, minv, fixed_iterations=20)
+        res = S.solve(variant, op, b, minv=minv, config=S.SolverConfig(fixed_iterations=20))
+        assert rel(hist_array(res.history)[:, 3], hist_array(hist)[:, 3]) < 1e-4, (p, variant)
+        assert rel(res.x, x) < 1e-4, (p, variant)
+    # the library's own diagonal (computed in fp64, applied in fp32) gives the same history
+    res2 = S.solve("combined_pcg", op, b, minv=op.compute_diagonal(), config=S.SolverConfig(fixed_iterations=20))
+    x, k, r, conv, hist = orc.combined_pcg(lambda v: orc.apply(prob, v), b, minv, fixed_iterations=20)
+    assert rel(hist_array(res2.history)[:, 3], hist_array(hist)[:, 3]) < 1e-4
+
+
+@pytest.mark.parametrize("p", range(1, 9))
 def test_all_degrees_apply_and_short_solve(p):
     S = _solvers()
     cells = {1: (19, 18, 5), 2: (11, 12, 4), 3: (7, 8, 3), 4: (6, 5, 3), 5: (5, 4, 3), 6: (4, 3, 3),
@@ -267,8 +292,12 @@ def test_curved_midsize_vs_oracle_and_errors():
     assert op.info()["geometry_bytes"] > 0
     with pytest.raises(ValueError):            # affine on a deformed mesh (mesh.py:214-216)
         gpu_operator(m, h, plan, p, nq, variant="affine")
-    with pytest.raises(NotImplementedError):   # n_q > p+1 on curved meshes is outside the GPU path
-        gpu_operator(m, h, plan, p, nq + 1, variant="final_tensor_load")
+    # n_q > p+1 on curved meshes (operator.py:69-70; BP3 / BP4 use p+2): the cell-by-cell path, every variant
+    for nq2 in (nq + 1, nq + 3):
+        prob2 = oracle_problem(m, h, p, nq2, geometry="curved")
+        ref2 = orc.apply(prob2, u)
+        for variant in ("final_tensor_load", "inverse_jacobian_load", "quadratic_compute"):
+            assert rel(gpu_operator(m, h, plan, p, nq2, variant=variant).apply(u), ref2) < 1e-12, (nq2, variant)
     # undeformed mesh: final-tensor variant == affine (reference tests/test_operator.py:90-95)
     m0, h0, plan0 = host_tables((5, 4, 3), 3)
     u0 = np.random.default_rng(9).standard_normal(h0.n_dofs)
@@ -410,3 +439,63 @@ def test_repeated_solves_on_ragged_brick_grid():
         worst = max(worst, float(np.max(np.abs(H - ref) / ref)))
     print(f"repeated ragged solves: max relative history deviation {worst:.2e}")
     assert worst < 1e-9   # run-to-run differences come from the order of the RED.F64 adds only
+
+
+@pytest.mark.parametrize("variant", ["final_tensor_load", "inverse_jacobian_load", "quadratic_compute"])
+def test_full_size_properties_curved(variant):
+    """BASELINE configs[2]: Q5 on 96^3 cells deformed by 0.1 sin sin sin (1.11e8 DoFs), each geometry variant.
+    No oracle runs there; size-independent properties as in test_full_size_properties, plus agreement of the
+    variants with each other through the residual history (the reference pins its variants to each other at
+    1e-12 on one apply, tests/test_operator.py:82-88)."""
+    S = _solvers()
+    p, n = 5, 96
+    m, h, plan = host_tables((n, n, n), p, deform=0.1)
+    op = gpu_operator(m, h, plan, p, p + 1, variant=variant)
+    b = seeded_rhs(h)
+    minv = op.compute_diagonal()
+    iters = 30
+    mer = S.solve("combined_pcg", op, b, minv=minv, config=S.SolverConfig(fixed_iterations=iters))
+    std = S.solve("pcg", op, b, minv=minv, config=S.SolverConfig(fixed_iterations=iters))
+    Hm, Hs = hist_array(mer.history), hist_array(std.history)
+    assert rel(Hm[:, 0], Hs[:, 0]) < 1e-8 and rel(Hm[:, 1], Hs[:, 1]) < 1e-8
+    assert rel(Hm[:, 3], Hs[:, 3]) < 1e-8
+    bn = np.linalg.norm(b)
+    Ax = op.apply(mer.x)
+    assert abs(np.linalg.norm(b - Ax) / bn - mer.residual) < 1e-9
+    assert np.array_equal(Ax[h.constrained_dofs], mer.x[h.constrained_dofs])
+    Ab = op.apply(b)
+    assert rel(op.apply(2.0 * mer.x - 3.0 * b), 2.0 * Ax - 3.0 * Ab) < 1e-12
+    assert abs(mer.x @ Ax - mer.x @ b) <= 2 * mer.residual * bn * np.linalg.norm(mer.x)
+    # symmetry: u.A w == w.A u
+    w = np.random.default_rng(9).standard_normal(h.n_dofs)
+    w[h.constrained_dofs] = 0.0
+    Aw = op.apply(w)
+    assert abs(b @ Aw - w @ Ab) <= 1e-11 * np.linalg.norm(b) * np.linalg.norm(Aw)
+    # all variants describe the same operator: the first residuals are pinned across variants
+    key = [float(v) for v in Hs[:5, 3]]
+    seen = _CURVED_SEEN.setdefault("hist", key)
+    assert rel(np.array(key), np.array(seen)) < 1e-10
+
+
+_CURVED_SEEN = {}
+
+
+@pytest.mark.parametrize("key", ["bp3", "bp4", "bp3_p2"])
+def test_bp_canonical_vs_reference(golden, key):
+    """BP3 / BP4 exactly as the reference's harness builds them (bench.py:153-187 defaults: mesh deformed by
+    0.05, final_tensor_load, n_q = p + 2 Gauss points) against fixtures generated by the unmodified reference
+    (oracle/make_golden.py::bp_canonical): manufactured RHS, one apply, the Jacobi diagonal at 1e-12, 25
+    iterations of pcg / combined_pcg."""
+    from paper_2205_08909_b200 import harness
+    S = _solvers()
+    g = golden["bp_canonical"]
+    bp, p, cells = {"bp3": ("BP3", 5, (3, 3, 3)), "bp4": ("BP4", 5, (2, 2, 3)), "bp3_p2": ("BP3", 2, (4, 3, 5))}[key]
+    op, b, minv = harness.assemble_problem(bp, p, cells)
+    assert op.spec.n_q_1d == p + 2
+    assert rel(b, g[f"{key}_b"]) < 1e-13
+    assert rel(op.apply(g[f"{key}_u"]), g[f"{key}_Au"]) < 1e-12
+    assert rel(minv.inverse_diagonal, g[f"{key}_invdiag"]) < 1e-12
+    for variant in ("pcg", "combined_pcg"):
+        res = S.solve(variant, op, g[f"{key}_b"], minv=minv, config=S.SolverConfig(fixed_iterations=25))
+        assert rel(hist_array(res.history), g[f"{key}_{variant}_hist"]) < 1e-10, variant
+        assert rel(res.x, g[f"{key}_{variant}_x"]) < 1e-10, variant

@@ -79,3 +79,18 @@ def test_manufactured_rhs_matches_reference(golden):
     b4 = harness.build_rhs(f)
     ref4 = golden["harness"]["bp4_p3_322_rhs"]
     assert b4.shape == ref4.shape and np.max(np.abs(b4 - ref4)) / np.max(np.abs(ref4)) < 1e-13
+
+
+def test_bench_csv_schema_matches_reference():
+    """Header and field formatting of the reference's `mfcg bench` CSV (cli.py:155-186): `repr` wall time,
+    %.6g floats, cells joined with x."""
+    from paper_2205_08909_b200 import harness as H
+    rec = H.RunRecord.from_run("BP5", 5, (4, 4, 4), 9261, "combined_pcg", 100, 0.0123456789, 1.5e-7)
+    text = H.write_bench_csv([rec])
+    head, row = text.strip().split("\n")
+    assert head == ("bp,degree,cells,n_dofs,variant,iterations,wall_time_s,throughput_dofs_per_s,final_residual,"
+                    "model_reads_per_dof,model_writes_per_dof")
+    f = row.split(",")
+    assert f[:6] == ["BP5", "5", "4x4x4", "9261", "combined_pcg", "100"]
+    assert f[6] == repr(0.0123456789) and f[7] == f"{9261 * 100 / 0.0123456789:.6g}" and f[8] == "1.5e-07"
+    assert [float(f[9]), float(f[10])] == [rec.reads_per_dof, rec.writes_per_dof]

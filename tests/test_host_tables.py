@@ -156,3 +156,33 @@ def test_three_component_numbering_matches_reference(golden):
         assert np.array_equal(h.constrained_dofs, g[f"v{ci}_constrained"])
         if numbering == "optimized":
             assert np.array_equal(h.permutation, g[f"v{ci}_permutation"])
+
+
+@pytest.mark.parametrize("n", [32, 48])
+def test_large_integer_tables_sha256(n):
+    """The vectorised numbering / renumbering / schedule at 32^3 and 48^3 cells Q5 (4.2e6 / 1.4e7 DoFs) against
+    SHA-256 digests of the reference's tables (tests/golden/big_tables.json, oracle/make_golden.py::
+    big_table_digests): bit-exact far beyond the 8^3 meshes whose arrays are committed."""
+    import hashlib
+    import json
+    from pathlib import Path
+    ref = json.loads((Path(__file__).parent / "golden" / "big_tables.json").read_text())[str(n)]
+
+    def dg(a):
+        a = np.ascontiguousarray(a)
+        return hashlib.sha256(a.tobytes()).hexdigest() + f":{a.dtype}:{a.shape}"
+
+    mesh = pmesh.build_cartesian_mesh((n, n, n))
+    h = dofs.distribute_dofs(mesh, 5, 1, constrain_boundary=True)
+    plan = dofs.make_batches(mesh, dofs.batch_size(5, 1, 8), "morton")
+    assert h.n_dofs == ref["n_dofs"]
+    assert dg(h.cell_index_blocks) == ref["blocks"]
+    assert dg(h.constrained_dofs) == ref["constrained"]
+    assert dg(np.concatenate([np.asarray(b) for b in plan.batches])) == ref["batches"]
+    hr = dofs.renumber_optimized(h, plan)
+    assert dg(hr.cell_index_blocks) == ref["ren_blocks"]
+    assert dg(hr.permutation) == ref["ren_permutation"]
+    assert dg(hr.constrained_dofs) == ref["ren_constrained"]
+    sch = dofs.compute_range_schedule(hr, plan)
+    assert dg(sch.first_touch_batch) == ref["schedule_first"]
+    assert dg(sch.last_touch_batch) == ref["schedule_last"]
