@@ -251,7 +251,7 @@ static int op_create_impl(mfcg_ctx* ctx, const mfcg_op_desc* d, mfcg_op* op) {
                ((g.cells[2] + z - 1) / z);
       };
       const char* env = std::getenv("MFCG_BRICK2");
-      const bool persistent = d->geometry == MFCG_GEOM_AFFINE && p >= 2 && p <= 5 && !(env && env[0] == '0');
+      const bool persistent = d->geometry == MFCG_GEOM_AFFINE && p >= 4 && p <= 5 && !(env && env[0] == '0');
       if (persistent) {
         // merged iterations run in the persistent kernel (mfcg_brick2.cuh): block i walks bricks i, i + SMs, ...
         // Pick the depth that minimises the layers of the busiest block, with ~0.7 layer per brick for the

@@ -89,8 +89,11 @@ template <int ID, int COUNT> __device__ __forceinline__ void named_arrive() {
 #endif
 
 template <int P> struct Brick2Enabled {
-  // needs a multiple of 16 cells per layer (cell-minor mapping) and N^2 * 2 values of a plane in registers
-  static constexpr bool value = (P >= 2 && P <= 5) && (Cfg<P, 0>::BX * Cfg<P, 0>::BY) % 16 == 0;
+  // needs a multiple of 16 cells per layer (cell-minor mapping) and N^2 * 2 values of a plane in registers.
+  // Measured at ~5e7 DoFs (profiles/r02_sweeps.txt): p = 5 +5 %, p = 4 +1 %, but p = 3 / 2 -13 / -10 % against
+  // the first-generation kernel (many small planes per layer: the per-plane hand-over costs more than the
+  // register-resident sweeps save), so the low degrees stay there.
+  static constexpr bool value = (P >= 4 && P <= 5) && (Cfg<P, 0>::BX * Cfg<P, 0>::BY) % 16 == 0;
 };
 
 template <int P, typename T> struct Geo2 {
