@@ -585,23 +585,22 @@ int mfcg_solve_group(mfcg_op** ops, int n_ops, const mfcg_solve_args* args, mfcg
   Ctx* c = ops[0]->common.ctx;
   cudaSetDevice(c->device);
   const mfcg_solve_args& a0 = args[0];
-  if (a0.variant != MFCG_COMBINED_PCG && a0.variant != MFCG_COMBINED_CG) {
-    set_error("slab groups run the merged variants (combined_cg / combined_pcg)");
-    return MFCG_EUNSUPPORTED;
-  }
+  if (a0.variant < 0 || a0.variant > 3) { set_error("unknown solver variant"); return MFCG_EINVAL; }
+  const bool merged = a0.variant == MFCG_COMBINED_PCG || a0.variant == MFCG_COMBINED_CG;
+  const bool with_prec = a0.variant == MFCG_COMBINED_PCG || a0.variant == MFCG_PCG;
   if (a0.tolerance <= 0 || a0.max_iterations < 1) { set_error("bad tolerance / max_iterations"); return MFCG_EINVAL; }
   const bool fixed = a0.fixed_iterations >= 0;
   const int limit = a0.fixed_iterations > 0 ? a0.fixed_iterations : a0.max_iterations;
   GroupScratch gs;
   if ((rc = gs.init())) return rc;
-  if (a0.variant == MFCG_COMBINED_PCG && !a0.inv_diag)
+  if (with_prec && !a0.inv_diag)
     if ((rc = group_diagonal(ops, n_ops, gs))) return rc;
   EventPair ev;  // destroyed on every return path
   MFCG_CUDA(ev.create());
   cudaEvent_t t0 = ev.a, t1 = ev.b;
   MFCG_CUDA(cudaEventRecord(t0, c->stream));
   for (int i = 0; i < n_ops; ++i)
-    if ((rc = ops[i]->engine->g_begin(&args[i], limit))) return rc;
+    if ((rc = merged ? ops[i]->engine->g_begin(&args[i], limit) : ops[i]->engine->g_std_begin(&args[i], limit))) return rc;
   if ((rc = group_sums(ops, n_ops, 1, gs.d_global))) return rc;
   double bb = 0.0;
   MFCG_CUDA(cudaMemcpyAsync(&bb, gs.d_global, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -610,6 +609,37 @@ int mfcg_solve_group(mfcg_op** ops, int n_ops, const mfcg_solve_args* args, mfcg
   if (bb > 0.0) {
     for (int i = 0; i < n_ops; ++i)
       if ((rc = ops[i]->engine->g_set_state(&args[i], limit, gs.d_global))) return rc;
+    if (!merged) {
+      // standard (P)CG, region by region (solvers.py:296-336): the operator with the plane exchange, three
+      // scalar all-reduces per iteration (p.v; r.r and r.z together) -- PAPER.md:7086-7088
+      for (int i = 0; i < n_ops; ++i)
+        if ((rc = ops[i]->engine->g_std_init_vectors())) return rc;
+      if ((rc = group_sums(ops, n_ops, 2, gs.d_global))) return rc;
+      for (int i = 0; i < n_ops; ++i)
+        if ((rc = ops[i]->engine->g_std_init_scalar(gs.d_global))) return rc;
+      for (int it = 1; it <= limit; ++it) {
+        for (int i = 0; i < n_ops; ++i)
+          if ((rc = ops[i]->engine->g_std_apply_front())) return rc;
+        if ((rc = group_finish_exchange(ops, n_ops, false, gs.ev))) return rc;
+        for (int i = 0; i < n_ops; ++i) {
+          if ((rc = ops[i]->engine->g_std_apply_end())) return rc;
+          if ((rc = ops[i]->engine->g_std_dot_pv())) return rc;
+        }
+        if ((rc = group_sums(ops, n_ops, 1, gs.d_global))) return rc;
+        for (int i = 0; i < n_ops; ++i) {
+          if ((rc = ops[i]->engine->g_std_alpha_update(gs.d_global))) return rc;
+          if ((rc = ops[i]->engine->g_std_dots_r())) return rc;
+        }
+        if ((rc = group_sums(ops, n_ops, 2, gs.d_global))) return rc;
+        for (int i = 0; i < n_ops; ++i)
+          if ((rc = ops[i]->engine->g_std_beta_p(gs.d_global))) return rc;
+        if (!fixed && (it % 8 == 0)) {
+          int active = 1;
+          if ((rc = ops[0]->engine->g_poll(&active))) return rc;
+          if (!active) break;
+        }
+      }
+    } else
     for (int it = 1; it <= limit; ++it) {
       for (int i = 0; i < n_ops; ++i)
         if ((rc = ops[i]->engine->g_front(false))) return rc;

@@ -101,6 +101,16 @@ struct EngineBase {
   virtual double* g_sums() = 0;
   virtual int g_apply_front(const double* src, int location) = 0;
   virtual int g_apply_end(double* dst, int location) = 0;
+  // standard (P)CG on slabs: the regions of solvers.py:296-336, dot products over owned DoFs
+  virtual int g_std_begin(const mfcg_solve_args* a, int limit) = 0;
+  virtual int g_std_init_vectors() = 0;
+  virtual int g_std_init_scalar(const double* global_sums_dev) = 0;
+  virtual int g_std_apply_front() = 0;
+  virtual int g_std_apply_end() = 0;
+  virtual int g_std_dot_pv() = 0;
+  virtual int g_std_alpha_update(const double* global_sums_dev) = 0;
+  virtual int g_std_dots_r() = 0;
+  virtual int g_std_beta_p(const double* global_sums_dev) = 0;
 };
 
 template <int P, typename T>
@@ -683,7 +693,7 @@ class Engine : public EngineBase {
     s0.active = 1;
     s0.fixed = a->fixed_iterations >= 0 ? 1 : 0;
     s0.force_x = a->force_x_updates ? 1 : 0;
-    s0.has_prec = a->variant == MFCG_COMBINED_PCG ? 1 : 0;
+    s0.has_prec = (a->variant == MFCG_COMBINED_PCG || a->variant == MFCG_PCG) ? 1 : 0;
     s0.limit = limit;
     s0.tol = a->tolerance;
     s0.residual = 1.0;
@@ -694,11 +704,128 @@ class Engine : public EngineBase {
     return MFCG_OK;
   }
 
+  // ---- standard (P)CG on a slab (BASELINE configs[3]/[4] arm "standard vs merged")
+  int g_std_begin(const mfcg_solve_args* a, int limit) override {
+    const i64 n = c_->grid.n_dofs;
+    int rc = g_alloc();
+    if (rc) return rc;
+    if (history_cap_ < limit) {
+      if (d_history_) cudaFree(d_history_);
+      MFCG_CUDA(cudaMalloc(&d_history_, sizeof(double) * 4 * (size_t)limit));
+      history_cap_ = limit;
+    }
+    launches_ = op_launches_ = 0;
+    time_kernels_ = false;
+    event_cursor_ = 0;
+    use_brick2_ = false;
+    tab_.diag_onfly = 0;
+    std_prec_ = a->variant == MFCG_PCG;
+    if ((rc = load_vec(a->b, a->location, v_))) return rc;   // b is staged in v, as in run_standard
+    if (std_prec_) {
+      if (a->inv_diag) {
+        if ((rc = load_vec(a->inv_diag, a->location, minv_))) return rc;
+      } else {
+        k_convert<T, double><<<vgrid_, VT, 0, stream()>>>(n, c_->d_invdiag, minv_);
+        ++launches_;
+      }
+    }
+    k_dot_owned<T><<<vgrid_, VT, 0, stream()>>>(c_->grid, v_, v_, partials_a_);
+    k_reduce_partials<<<1, 256, 0, stream()>>>(partials_a_, vgrid_, 1, 0, d_sums_);   // b.b of this slab
+    launches_ += 2;
+    MFCG_CUDA(cudaGetLastError());
+    return MFCG_OK;
+  }
+  // after g_set_state: r = b, z = M r, p = z, x = 0 and this slab's r.z, r.r
+  int g_std_init_vectors() override {
+    k_std_init_owned<T><<<vgrid_, VT, 0, stream()>>>(c_->grid, v_, std_prec_ ? minv_ : nullptr, r_, z_, p_, x_, partials_a_);
+    k_reduce_partials<<<1, 256, 0, stream()>>>(partials_a_, vgrid_, 2, 0, d_sums_);
+    launches_ += 2;
+    MFCG_CUDA(cudaGetLastError());
+    return MFCG_OK;
+  }
+  int g_std_init_scalar(const double* global_sums_dev) override {
+    k_std_init_scalar<<<1, 256, 0, stream()>>>(global_sums_dev, 1, c_->d_state);  // one row: r.z, r.r
+    ++launches_;
+    MFCG_CUDA(cudaGetLastError());
+    return MFCG_OK;
+  }
+  int g_std_apply_front() override {
+    const BrickGrid& g = c_->grid;
+    const i64 nb = c_->n_bricks, nxy = (i64)g.mb[0] * g.mb[1];
+    int rc;
+    if (g.n_dofs > g.n_int) {
+      k_surface_init<T><<<vgrid_, VT, 0, stream()>>>(g, v_);
+      ++launches_;
+    }
+    if (g.mb[2] <= 2) {
+      if ((rc = launch_brick(0, p_, nullptr, v_, nullptr))) return rc;
+      MFCG_CUDA(cudaEventRecord(ev_front_, stream()));
+    } else {
+      if ((rc = launch_brick(0, p_, nullptr, v_, nullptr, 0, nxy))) return rc;
+      if ((rc = launch_brick(0, p_, nullptr, v_, nullptr, nb - nxy, nxy))) return rc;
+      MFCG_CUDA(cudaEventRecord(ev_front_, stream()));
+      if ((rc = launch_brick(0, p_, nullptr, v_, nullptr, nxy, nb - 2 * nxy))) return rc;
+    }
+    MFCG_CUDA(cudaStreamWaitEvent(c_->ctx->comm_stream, ev_front_, 0));
+    return pack_planes(false);
+  }
+  int g_std_apply_end() override {
+    const BrickGrid& g = c_->grid;
+    if (g.n_dofs > g.n_int) {
+      k_surface_fix<T><<<vgrid_, VT, 0, stream()>>>(g, p_, v_);
+      ++launches_;
+    }
+    MFCG_CUDA(cudaGetLastError());
+    return MFCG_OK;
+  }
+  int g_std_dot_pv() override {
+    k_dot_owned<T><<<vgrid_, VT, 0, stream()>>>(c_->grid, p_, v_, partials_a_);
+    k_reduce_partials<<<1, 256, 0, stream()>>>(partials_a_, vgrid_, 1, 0, d_sums_);
+    launches_ += 2;
+    MFCG_CUDA(cudaGetLastError());
+    return MFCG_OK;
+  }
+  int g_std_alpha_update(const double* global_sums_dev) override {
+    const i64 n = c_->grid.n_dofs;
+    k_std_alpha<<<1, 256, 0, stream()>>>(global_sums_dev, 1, c_->d_state);
+    k_std_axpy<T><<<vgrid_, VT, 0, stream()>>>(n, x_, p_, 1.0, c_->d_state);
+    k_std_axpy<T><<<vgrid_, VT, 0, stream()>>>(n, r_, v_, -1.0, c_->d_state);
+    launches_ += 3;
+    MFCG_CUDA(cudaGetLastError());
+    return MFCG_OK;
+  }
+  // this slab's r.r (sum 0) and r.z (sum 1; = r.r without preconditioner)
+  int g_std_dots_r() override {
+    const i64 n = c_->grid.n_dofs;
+    k_dot_owned<T><<<vgrid_, VT, 0, stream()>>>(c_->grid, r_, r_, partials_a_);
+    k_reduce_partials<<<1, 256, 0, stream()>>>(partials_a_, vgrid_, 1, 0, d_sums_);
+    launches_ += 2;
+    if (std_prec_) {
+      k_std_prec<T><<<vgrid_, VT, 0, stream()>>>(n, z_, minv_, r_, c_->d_state);
+      k_dot_owned<T><<<vgrid_, VT, 0, stream()>>>(c_->grid, r_, z_, partials_b_);
+      k_reduce_partials<<<1, 256, 0, stream()>>>(partials_b_, vgrid_, 1, 0, d_sums_ + 1);
+      launches_ += 3;
+    }
+    MFCG_CUDA(cudaGetLastError());
+    return MFCG_OK;
+  }
+  // global_sums_dev: row 0 = (r.r, r.z)
+  int g_std_beta_p(const double* global_sums_dev) override {
+    const i64 n = c_->grid.n_dofs;
+    k_std_beta_sums<<<1, 32, 0, stream()>>>(global_sums_dev, std_prec_ ? 1 : 0, c_->d_state, d_history_);
+    k_std_update_p<T><<<vgrid_, VT, 0, stream()>>>(n, p_, std_prec_ ? z_ : r_, c_->d_state);
+    launches_ += 2;
+    MFCG_CUDA(cudaGetLastError());
+    return MFCG_OK;
+  }
+
   int g_end(const mfcg_solve_args* a, mfcg_solve_result* res) override {
     std::memset(res, 0, sizeof(*res));
     const i64 n = c_->grid.n_dofs;
-    k_finalize_x<T><<<vgrid_, VT, 0, stream()>>>(nt_, x_, p_, r_, minv_, c_->d_state);
-    ++launches_;
+    if (a->variant == MFCG_COMBINED_CG || a->variant == MFCG_COMBINED_PCG) {  // x catch-up of the merged loop
+      k_finalize_x<T><<<vgrid_, VT, 0, stream()>>>(nt_, x_, p_, r_, minv_, c_->d_state);
+      ++launches_;
+    }
     int rc = store_vec(x_, a->x, a->location);
     if (rc) return rc;
     MFCG_CUDA(cudaMemcpyAsync(c_->h_state, c_->d_state, sizeof(SolveState), cudaMemcpyDeviceToHost, stream()));
@@ -838,6 +965,7 @@ class Engine : public EngineBase {
   PointTab qpt_{};
   int cell_smem_ = 0;
   bool brick2_ok_ = false, use_brick2_ = false;
+  bool std_prec_ = false;  // slab-group standard solve: with Jacobi preconditioner
   void* plane_[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [side lo/hi][send/recv]
   double* d_sums_ = nullptr;
   double* diag_raw_ = nullptr;  // slab runs: diagonal before the interface exchange

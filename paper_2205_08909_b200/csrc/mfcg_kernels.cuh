@@ -1656,6 +1656,27 @@ static __global__ void k_std_beta(const double* __restrict__ rr_partials, const 
   if (k >= st->limit) st->active = 0;
 }
 
+// slab runs: sums[0] = r.r, sums[1] = r.z already reduced over all slabs / ranks
+static __global__ void k_std_beta_sums(const double* __restrict__ sums, int prec, SolveState* st,
+                                       double* __restrict__ history) {
+  if (!st->active || threadIdx.x != 0) return;
+  const double rr = sums[0];
+  const double gamma_new = prec ? sums[1] : rr;
+  const double residual = sqrt(rr) / st->bnorm;
+  const double beta = st->gamma > 0.0 ? gamma_new / st->gamma : 0.0;
+  const int k = st->k + 1;
+  history[(i64)(k - 1) * 4 + 0] = st->alpha;
+  history[(i64)(k - 1) * 4 + 1] = beta;
+  history[(i64)(k - 1) * 4 + 2] = st->gamma;
+  history[(i64)(k - 1) * 4 + 3] = residual;
+  st->gamma = gamma_new;
+  st->beta = beta;
+  st->residual = residual;
+  st->k = k;
+  if (!st->fixed && residual < st->tol) { st->converged = 1; st->active = 0; }
+  if (k >= st->limit) st->active = 0;
+}
+
 // p = beta p + z.  Runs even on the iteration that hit the limit in the
 // reference (solvers.py:334-335 executes unless the loop broke on convergence);
 // p is not observable afterwards, so skipping it when inactive is equivalent.
@@ -1792,6 +1813,26 @@ __global__ void k_dot_owned(BrickGrid g, const T* __restrict__ a, const T* __res
   }
   block_reduce7_store(s, red, partials + (i64)blockIdx.x * 8);
 }
+// standard (P)CG on a slab: r = b, z = M r, p = z, x = 0; sums of r.z (col 0) and r.r (col 1) over owned DoFs
+template <typename T>
+__global__ void k_std_init_owned(BrickGrid g, const T* __restrict__ B, const T* __restrict__ Minv, T* __restrict__ R,
+                                 T* __restrict__ Z, T* __restrict__ Pv, T* __restrict__ X, double* __restrict__ partials) {
+  __shared__ double red[7 * 32];
+  double s[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < g.n_dofs; i += (i64)gridDim.x * blockDim.x) {
+    const T r = B[i];
+    const T z = Minv ? Minv[i] * r : r;
+    R[i] = r;
+    if (Minv) Z[i] = z;
+    Pv[i] = z;
+    X[i] = (T)0;
+    if (i >= g.n_int && (g.mask[i - g.n_int] & 2)) continue;  // ghost copy: counted by the lower slab
+    s[0] += (double)r * (double)z;
+    s[1] += (double)r * (double)r;
+  }
+  block_reduce7_store(s, red, partials + (i64)blockIdx.x * 8);
+}
+
 // state for a slab run is written by the host; this sets the norm all slabs share
 static __global__ void k_set_bnorm(SolveState* st, const double* __restrict__ sums) { st->bnorm = sqrt(sums[0]); }
 

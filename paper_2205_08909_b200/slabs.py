@@ -128,7 +128,8 @@ class SlabGroup:
         return outs
 
     def solve(self, variant, bs, config=None, *, location=0, xs=None):
-        """Merged (P)CG on the whole mesh; returns one SolveResult per slab (same history)."""
+        """(P)CG on the whole mesh, merged (`combined_cg`, `combined_pcg`) or standard (`cg`, `pcg`); returns one
+        SolveResult per slab (same history)."""
         from .solvers import SolveResult, SolverBreakdown, SolverConfig, _BREAKDOWN_TEXT
         cfg = config or SolverConfig()
         n = len(self.ops)

@@ -142,6 +142,15 @@ def test_slab_group_equals_single_slab_on_one_gpu(cells, p, G, deform):
         assert r.iterations == 40
         assert rel(hist_array(r.history)[:30], H1[:30]) < 1e-10
         assert rel(r.x, one.x[gl]) < 1e-9
+    # standard (unfused) PCG and CG on the slabs (BASELINE configs[3]/[4] "standard vs merged" arm)
+    for variant in ("pcg", "cg"):
+        one_s = S.solve(variant, op1, b, minv=op1.compute_diagonal() if variant == "pcg" else None, config=cfg)
+        many_s = group.solve(variant, [b[gl] for gl in maps], cfg)
+        Hs = hist_array(one_s.history)
+        for gl, r in zip(maps, many_s):
+            assert r.iterations == 40 and r.matvecs == 40
+            assert rel(hist_array(r.history)[:30], Hs[:30]) < 1e-10, variant
+            assert rel(r.x, one_s.x[gl]) < 1e-9, variant
     # tolerance-terminated run agrees on the iteration count
     one = S.solve("combined_pcg", op1, b, minv=op1.compute_diagonal(), config=S.SolverConfig(tolerance=1e-7))
     many = group.solve("combined_pcg", [b[gl] for gl in maps], S.SolverConfig(tolerance=1e-7))
