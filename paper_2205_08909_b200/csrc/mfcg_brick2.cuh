@@ -68,7 +68,7 @@ template <int ID, int COUNT> __device__ __forceinline__ void named_arrive() {
 #define MFCG_B2_NT 5   // transient plane slots (p, v, x)
 #endif
 #ifndef MFCG_B2_RLAYERS
-#define MFCG_B2_RLAYERS 2  // layers of lattice planes in the ring: the update runs RLAYERS - 1 layers ahead of the gather
+#define MFCG_B2_RLAYERS 3  // layers of lattice planes in the ring: the update runs RLAYERS - 1 layers ahead of the gather
 #endif
 #ifndef MFCG_B2_UNR
 #define MFCG_B2_UNR 2
@@ -151,8 +151,7 @@ template <int P, typename T> struct Geo2 {
   static constexpr size_t OFF_DTAB = al(OFF_T + sizeof(T) * NT * 3 * PLB);
   static constexpr size_t OFF_GTAB = al(OFF_DTAB + sizeof(T) * P * P * P);
   static constexpr size_t OFF_ITAB = al(OFF_GTAB + 8 * (size_t)FP_MAX);
-  static constexpr size_t OFF_MSUM = al(OFF_ITAB + 2 * (size_t)NINT2D);   // per math thread: the five sums of the brick
-  static constexpr size_t SMEM = al(OFF_MSUM + 8 * 5 * (size_t)NLM);
+  static constexpr size_t SMEM = al(OFF_ITAB + 2 * (size_t)NINT2D);
   static_assert(SMEM <= 232448 - 1024, "shared memory of the persistent brick kernel");
 };
 
@@ -189,7 +188,6 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
   T* const dtab = reinterpret_cast<T*>(smem_raw + G2::OFF_DTAB);
   uint2* const gtab = reinterpret_cast<uint2*>(smem_raw + G2::OFF_GTAB);
   unsigned short* const itab = reinterpret_cast<unsigned short*>(smem_raw + G2::OFF_ITAB);
-  double* const msum = reinterpret_cast<double*>(smem_raw + G2::OFF_MSUM);
 
   const int tid = threadIdx.x;
   if (!st->active) return;
@@ -256,10 +254,8 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
   const i64 n_int = g.n_int;
   (void)n_int;
 
-  // math warps: sums that need v (p.v, r.v, v.v, r.Mv, v.Mv) are kept per thread in shared memory between
-  // the layers (the registers belong to stage 1); the update warps hand over r.r and r.Mr per layer
-  if (tid < NLM)
-    for (int i = 0; i < 5; ++i) msum[i * NLM + tid] = 0.0;
+  // gather group: the sums that need v (p.v, r.v, v.v, r.Mv, v.Mv) stay in registers over a brick; the update
+  // warps hand over r.r and r.Mr with the brick's last layer
   if (tid == 0) { H.bsum[0] = 0.0; H.bsum[1] = 0.0; }  // running r.r, r.Mr of the brick
 
   // One brick loop per role, each entirely inside its own branch (ptxas allocates registers per
@@ -348,6 +344,8 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
         const unsigned sel = d.y >> 22;
         ppstride = ((sel & 1u) ? Lx - 1 : 1) * ((sel & 2u) ? Ly - 1 : 1);
       }
+      const i64 pbase1 = s27[pe2 + 9] + po2 - ppstride;  // planes 0 < K < Lz: pbase1 + ppstride * K
+      const bool bnd_xy = mx == 0 || mx == g.mb[0] - 1 || my == 0 || my == g.mb[1] - 1;
       double ls0 = 0.0, ls4 = 0.0;  // r.r and r.Mr of this thread over the brick
       for (int L = 0; L < bcz; ++L) {
         const int gl = g_base + L;
@@ -361,6 +359,9 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
         unsigned pmk[P + 1];  // mask bytes of this thread's perimeter position, consumed after the planes
 #pragma unroll
         for (int kk = 0; kk < P + 1; ++kk) pmk[kk] = 0;
+        // Dirichlet DoFs lie on the domain boundary (enforced at operator creation): only bricks that touch it
+        // need the mask bytes
+        const bool need_mask = bnd_xy || (mz == 0 && L == 0) || (mz == g.mb[2] - 1 && L == bcz - 1);
         if (ut < nperim) {
           const int nk = P + 1 - k0;
 #pragma unroll
@@ -368,13 +369,13 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
             if (kk >= nk) break;
             const int K = L * P + k0 + kk;
             const int ez = K == 0 ? 0 : (K == Lz ? 2 : 1);
-            const i64 gi = s27[pe2 + 9 * ez] + po2 + (ez == 1 ? (i64)ppstride * (K - 1) : 0);
+            const i64 gi = ez == 1 ? pbase1 + (i64)ppstride * K : s27[pe2 + 9 * ez] + po2;
             MFCG_CHECK(gi >= n_int && gi < g.n_dofs && pcw < PLANE && K <= Lz);
             const int dst = ((kb_base + K) % RB) * PLANE + pcw;
             // asynchronous copy straight into the ring (LDGSTS); constrained points are zeroed afterwards
             asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(ring + dst)), "l"(Pv + gi),
                          "n"((int)sizeof(T)) : "memory");
-            pmk[kk] = g.mask[gi - n_int];
+            if (need_mask) pmk[kk] = g.mask[gi - n_int];
           }
         }
         B2_TOC(tu, 3);
@@ -517,11 +518,12 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
           T* pl = ring + ((kb_base + (side == 0 ? 0 : Lz)) % RB) * PLANE;
           unsigned fbits = 0;
           int cnt = 0;
+          const bool face_mask = side == 0 ? mz == 0 : mz == g.mb[2] - 1;  // the face lies on the domain boundary
           for (int it = ut; it < nint2d; it += NUPD, ++cnt) {
             MFCG_CHECK(fb + it >= n_int && fb + it < g.n_dofs);
             asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(pl + (itab[it] & 1023u))),
                          "l"(Pv + fb + it), "n"((int)sizeof(T)) : "memory");
-            fbits |= (unsigned)(g.mask[fb + it - n_int] & 1) << cnt;
+            if (face_mask) fbits |= (unsigned)(g.mask[fb + it - n_int] & 1) << cnt;
           }
           asm volatile("cp.async.wait_all;" ::: "memory");
           cnt = 0;
@@ -631,6 +633,7 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
       for (int i = lt; i < PLANE; i += NLM) carry[i] = (T)0;
       named_barrier<1, NLM>();
       const i64 st_int = s27[13];
+      double s1 = 0, s2 = 0, s3 = 0, s5 = 0, s6 = 0;
       for (int L = 0; L < bcz; ++L) {
         const int gl = g_base + L;
         const int sl0 = (kb_base + L * P) % RB;
@@ -679,7 +682,6 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
 #pragma unroll
         for (int k = 0; k < P; ++k) rso[k] = ((sl0 + k) % RB) * PLANE;
         // the five sums of a finished DoF, on r', p' and 1/diag that stayed on chip (solvers.py:692-698)
-        double s1 = 0, s2 = 0, s3 = 0, s5 = 0, s6 = 0;
         auto post = [&](T r_, T p_, T m_, T v_) {
           const double r = (double)r_, p = (double)p_, m = (double)m_, v = (double)v_;
           const double mv = m * v;
@@ -753,17 +755,12 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
         }
         mbar_arrive(&H.ldone[gl & 3]);
         named_arrive<4, NS1 + NLM>();  // tiles free for the next layer
-        msum[0 * NLM + lt] += s1; msum[1 * NLM + lt] += s2; msum[2 * NLM + lt] += s3;
-        msum[3 * NLM + lt] += s5; msum[4 * NLM + lt] += s6;
         B2_TOC(tm, 2);
       }
       // brick sums, fixed order (deterministic)
       {
-        double sm[7] = {0.0, msum[0 * NLM + lt], msum[1 * NLM + lt], msum[2 * NLM + lt], 0.0,
-                        msum[3 * NLM + lt], msum[4 * NLM + lt]};
+        double sm[7] = {0.0, s1, s2, s3, 0.0, s5, s6};
         if (lt == 0) { sm[0] = H.bsum[0]; sm[4] = H.bsum[1]; H.bsum[0] = 0.0; H.bsum[1] = 0.0; }
-#pragma unroll
-        for (int i = 0; i < 5; ++i) msum[i * NLM + lt] = 0.0;
         warp_reduce7(sm);
         named_barrier<1, NLM>();  // the previous brick's row has been written
         if ((lt & 31) == 0)
