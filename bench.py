@@ -162,6 +162,37 @@ class CpuPort:
         return time.perf_counter() - t0
 
 
+def reference_package_config1():
+    """the reference package itself (pure Python / NumPy, sequential) on BASELINE
+    configs[0] -- 8^3 cells Q4, 100 fixed iterations -- when /root/reference is present (the authoring container);
+    the GPU box has no copy of it, and the entry says so."""
+    src = Path("/root/reference/pkg/src")
+    if not src.exists():
+        return {"available": False, "note": "/root/reference does not exist on this box; measured in the authoring "
+                                            "container: profiles/r02_reference_package_config1.json"}
+    sys.path.insert(0, str(src))
+    from mfcg.dofs import batch_size, distribute_dofs, make_batches
+    from mfcg.mesh import GeometryVariant, build_cartesian_mesh
+    from mfcg.operator import MatrixFreeOperator, OperatorSpec
+    from mfcg.solvers import SolverConfig, solve
+    mesh = build_cartesian_mesh((8, 8, 8))
+    h = distribute_dofs(mesh, 4, 1, constrain_boundary=True)
+    plan = make_batches(mesh, batch_size(4, 1, 8), "morton")
+    op = MatrixFreeOperator(OperatorSpec("laplace", 1, 4, 5, GeometryVariant.AFFINE, "gauss"), mesh, h, plan)
+    minv = op.compute_diagonal()
+    b = np.random.default_rng(0).uniform(-1, 1, h.n_dofs)
+    b[h.constrained_dofs] = 0.0
+    out = {"available": True, "config": "BASELINE configs[0]: 8^3 cells Q4, 35937 DoFs, 100 fixed iterations, one core"}
+    for variant in ("pcg", "combined_pcg"):
+        best = 1e30
+        for _ in range(3):
+            t0 = time.perf_counter()
+            res = solve(variant, op, b, minv=minv, config=SolverConfig(fixed_iterations=100))
+            best = min(best, time.perf_counter() - t0)
+        out[variant] = {"seconds": best, "DoF_it_per_s": h.n_dofs * 100 / best, "residual": res.residual}
+    return out
+
+
 def run_reference(args, rank):
     """The reference arm: the CPU port of the reference's merged Jacobi-PCG on the host cores, on the
     SAME mesh as the GPU arm (BASELINE configs[1] top rung at N = 1), for `--ref-iters` iterations per
@@ -190,6 +221,7 @@ def run_reference(args, rank):
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": port.cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
+        "reference_package_config1": reference_package_config1(),
     }
     print(json.dumps(line))
 
