@@ -290,8 +290,14 @@ def _cell_batch_ids(plan: BatchPlan, n_cells: int) -> np.ndarray:
 # renumbering
 
 
-def renumber_optimized(handler: DofHandler, plan: BatchPlan) -> DofHandler:
+def renumber_optimized(handler: DofHandler, plan: BatchPlan, remote_shared=None) -> DofHandler:
     """Locality renumbering of the batched cell loop (reference dofs.py:304-375).
+
+    ``remote_shared`` (scalar node ids, default none): nodes shared with other processes.  The reference keeps
+    category 2 for them "structurally present, always empty in this single-process build" (dofs.py:307-310,
+    331, 354); the z-slab decomposition fills it with the interface planes, ordered like
+    the reference orders that category: by (first batch, last batch, old start).  Without it the result is
+    the reference's, bit for bit.
 
     Entity categories: (0) touched by exactly one batch, ordered by
     (batch, old start); (1) touched by several batches, ordered by
@@ -335,6 +341,14 @@ def renumber_optimized(handler: DofHandler, plan: BatchPlan) -> DofHandler:
         raise ValueError("partially constrained entity cannot keep contiguous blocks")
     is_con = cmask[ent_start]
     cat = np.where(is_con, 3, np.where(ent_first == ent_last, 0, 1))
+    if remote_shared is not None and len(remote_shared):
+        rmask = np.zeros(n_nodes, dtype=bool)
+        rmask[np.asarray(remote_shared, dtype=np.int64)] = True
+        rsum = np.concatenate(([0], np.cumsum(rmask)))
+        rcov = rsum[ent_start + ent_size] - rsum[ent_start]
+        if np.any((rcov > 0) & (rcov < ent_size)):
+            raise ValueError("partially remote-shared entity cannot keep contiguous blocks")
+        cat = np.where((rcov > 0) & ~is_con, 2, cat)
 
     # one composite sort: category, then the category's own three keys
     k1 = np.where(cat == 1, -(ent_first + ent_last), ent_first)

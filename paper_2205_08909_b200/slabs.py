@@ -23,7 +23,7 @@ from . import _lib, dofs
 from .dofs import DofHandler
 from .mesh import HexMesh, build_cartesian_mesh
 
-__all__ = ["slab_layers", "Slab", "build_slab", "interface_plane_nodes", "SlabGroup"]
+__all__ = ["slab_layers", "Slab", "build_slab", "renumber_slab", "interface_plane_nodes", "SlabGroup"]
 
 
 def slab_layers(nz: int, n_slabs: int):
@@ -88,6 +88,23 @@ def build_slab(global_mesh: HexMesh, p: int, z0: int, nz_g: int, constrain_bound
         constrained = np.unique(node[on])
     h = DofHandler(h.n_dofs, 1, p, mesh.cells_per_dim, h.cell_index_blocks, constrained)
     return Slab(mesh, h, z0, nz, glob)
+
+
+def renumber_slab(slab: Slab, plan) -> Slab:
+    """`renumber_optimized` on a slab with its interface planes in the remote-shared category (SURVEY.md 8e;
+    the reference's placeholder dofs.py:307-310): unknowns touched by one batch first, then those shared between
+    batches, then the planes shared with the neighbouring slabs (contiguous: PAPER.md:6247-6253), the Dirichlet
+    unknowns last.  `global_nodes` follows the permutation."""
+    remote = []
+    if slab.has_lower:
+        remote.append(interface_plane_nodes(slab, "lower"))
+    if slab.has_upper:
+        remote.append(interface_plane_nodes(slab, "upper"))
+    remote = np.concatenate(remote) if remote else np.empty(0, dtype=np.int64)
+    h = dofs.renumber_optimized(slab.handler, plan, remote_shared=remote)
+    glob = np.empty_like(slab.global_nodes)
+    glob[h.permutation] = slab.global_nodes
+    return Slab(slab.mesh, h, slab.z0, slab.global_cells_z, glob)
 
 
 def interface_plane_nodes(slab: Slab, side: str) -> np.ndarray:

@@ -103,6 +103,41 @@ def test_slab_host_logic_world_size_2_gloo():
     assert results == [(0, True), (1, True)]
 
 
+@pytest.mark.parametrize("cells,p,G", [((4, 3, 8), 3, 2), ((3, 3, 9), 2, 3), ((2, 2, 8), 5, 4)])
+def test_slab_renumbering_with_remote_category(cells, p, G):
+    """Per-slab `renumber_optimized` with the interface planes in the remote-shared category (the reference's
+    empty placeholder, dofs.py:307-310): bijection, category order single-batch < multi-batch < remote <
+    constrained, the planes contiguous, and -- the oracle of SURVEY.md 8e -- the same relative order as the
+    plain renumbering inside every category."""
+    m, _ = _global(cells, p)
+    for z0, n in slabs.slab_layers(cells[2], G):
+        s = slabs.build_slab(m, p, z0, n)
+        plan = dofs.make_batches(s.mesh, dofs.batch_size(p, 1, 8), "morton")
+        r = slabs.renumber_slab(s, plan)
+        h, hr = s.handler, r.handler
+        perm = hr.permutation
+        assert np.array_equal(np.sort(perm), np.arange(h.n_dofs))
+        assert np.array_equal(np.sort(r.global_nodes), np.sort(s.global_nodes))
+        assert np.array_equal(r.global_nodes[perm], s.global_nodes)
+        # expansions follow the permutation (reference tests/test_dofs.py:214-221)
+        cells_all = np.arange(h.n_cells)
+        assert np.array_equal(dofs.expand_batch(hr, cells_all), perm[dofs.expand_batch(h, cells_all)])
+        # constrained tail, remote block right before it, contiguous
+        k = len(h.constrained_dofs)
+        assert np.array_equal(hr.constrained_dofs, np.arange(h.n_dofs - k, h.n_dofs))
+        planes = [slabs.interface_plane_nodes(s, side) for side, has in (("lower", s.has_lower), ("upper", s.has_upper)) if has]
+        remote = np.concatenate(planes) if planes else np.empty(0, dtype=np.int64)
+        con = np.zeros(h.n_dofs, bool)
+        con[h.constrained_dofs] = True
+        free_remote = remote[~con[remote]]
+        new_remote = np.sort(perm[free_remote])
+        assert np.array_equal(new_remote, np.arange(h.n_dofs - k - len(free_remote), h.n_dofs - k))
+        # same relative order as the plain renumbering among the unknowns that are neither remote nor constrained
+        plain = dofs.renumber_optimized(h, plan).permutation
+        rest = np.setdiff1d(np.arange(h.n_dofs), np.concatenate([free_remote, h.constrained_dofs]))
+        assert np.array_equal(np.argsort(plain[rest]), np.argsort(perm[rest]))
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("cells,p,G,deform", [((5, 4, 9), 5, 2, 0.0), ((6, 5, 12), 3, 3, 0.0),
                                               ((4, 4, 17), 5, 4, 0.0), ((4, 3, 6), 3, 2, 0.1)])
@@ -118,6 +153,8 @@ def test_slab_group_equals_single_slab_on_one_gpu(cells, p, G, deform):
     glob_of_lat = np.empty_like(lat)
     glob_of_lat[lat] = np.arange(h.n_dofs)
     sl = [slabs.build_slab(m, p, z0, n) for z0, n in slabs.slab_layers(cells[2], G)]
+    if G == 3:  # one case with per-slab optimized numbering (interface planes in the remote-shared category)
+        sl = [slabs.renumber_slab(s, dofs.make_batches(s.mesh, dofs.batch_size(p, 1, 8), "morton")) for s in sl]
     ops = []
     for s in sl:
         plan_s = dofs.make_batches(s.mesh, dofs.batch_size(p, 1, 8), "morton")
