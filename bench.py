@@ -322,12 +322,13 @@ def run_slabs(args, rank, local_rank, world):
     clocks = sampler.stop()
     # end to end through SlabGroup.solve with HOST buffers: every step copies the rank's part of b from pinned
     # host memory and x back (inside the library call); wall clock between barriers, max over ranks
-    group.solve(args.variant, [b_host.numpy()], cfg)
+    x_host = torch.empty(n_local, dtype=torch.float64).pin_memory()
+    group.solve(args.variant, [b_host.numpy()], cfg, outs=[x_host.numpy()])
     torch.cuda.synchronize()
     dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        group.solve(args.variant, [b_host.numpy()], cfg)
+        group.solve(args.variant, [b_host.numpy()], cfg, outs=[x_host.numpy()])
     torch.cuda.synchronize()
     dist.barrier()
     te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
@@ -388,6 +389,9 @@ def main():
     ap.add_argument("--cpu-baseline-cells", type=int, default=48,
                     help="edge of the cube the cpu_baseline leg of the GPU arm times (bounded sample)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-slabs", action="store_true",
+                    help="run the N > 1 code path (slab group, NCCL communicator, all-reduce) with one rank: a "
+                         "one-GPU check of everything but the cross-rank transfers")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -415,7 +419,10 @@ def main():
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} does not match WORLD_SIZE {world}")
     torch.cuda.set_device(local_rank)
-    if world > 1:
+    if world > 1 or args.force_slabs:
+        if world == 1:  # stand-alone rendezvous for the one-rank check
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
         run_slabs(args, rank, local_rank, world)
         return
     from paper_2205_08909_b200 import _lib

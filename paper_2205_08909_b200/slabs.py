@@ -144,9 +144,10 @@ class SlabGroup:
         _lib.check(self._lib.mfcg_diagonal_group(self._handles, len(self.ops), self._ptr_array(outs), 0))
         return outs
 
-    def solve(self, variant, bs, config=None, *, location=0, xs=None):
+    def solve(self, variant, bs, config=None, *, location=0, xs=None, minvs=None, outs=None):
         """(P)CG on the whole mesh, merged (`combined_cg`, `combined_pcg`) or standard (`cg`, `pcg`); returns one
-        SolveResult per slab (same history)."""
+        SolveResult per slab (same history).  ``minvs``: one caller-supplied inverse diagonal per slab (host arrays,
+        one value per node) instead of the operator's own Jacobi diagonal."""
         from .solvers import SolveResult, SolverBreakdown, SolverConfig, _BREAKDOWN_TEXT
         cfg = config or SolverConfig()
         n = len(self.ops)
@@ -160,7 +161,9 @@ class SlabGroup:
                 b = np.ascontiguousarray(bs[g], dtype=np.float64)
                 if len(b) != op.n_dofs:
                     raise ValueError("right-hand side length does not match operator")
-                x = np.empty(op.n_dofs)
+                x = outs[g] if outs is not None else np.empty(op.n_dofs)   # `outs`: e.g. pinned host arrays
+                if len(x) != op.n_dofs or x.dtype != np.float64 or not x.flags.c_contiguous:
+                    raise ValueError("output array must be contiguous float64 of the operator's length")
                 keep.append(b)
                 a.b, a.x = b.ctypes.data, x.ctypes.data
                 outs.append(x)
@@ -168,6 +171,14 @@ class SlabGroup:
                 a.b, a.x = int(bs[g]), int(xs[g])
                 outs.append(None)
             a.inv_diag = None
+            if minvs is not None:
+                if location != 0:
+                    raise ValueError("caller-supplied preconditioners are host arrays (location=0)")
+                md = np.ascontiguousarray(getattr(minvs[g], "inverse_diagonal", minvs[g]), dtype=np.float64)
+                if len(md) != op.n_dofs:
+                    raise ValueError("preconditioner length does not match operator")
+                keep.append(md)
+                a.inv_diag = md.ctypes.data
             a.variant = _lib.VARIANT_CODES[variant]
             a.location = location
             a.tolerance = cfg.tolerance

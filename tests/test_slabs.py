@@ -179,6 +179,10 @@ def test_slab_group_equals_single_slab_on_one_gpu(cells, p, G, deform):
         assert r.iterations == 40
         assert rel(hist_array(r.history)[:30], H1[:30]) < 1e-10
         assert rel(r.x, one.x[gl]) < 1e-9
+    # caller-supplied preconditioner per slab (the single-slab diagonal restricted to the slab)
+    custom = group.solve("combined_pcg", [b[gl] for gl in maps], cfg, minvs=[dref[gl] for gl in maps])
+    for gl, r in zip(maps, custom):
+        assert rel(hist_array(r.history)[:30], H1[:30]) < 1e-10
     # standard (unfused) PCG and CG on the slabs (BASELINE configs[3]/[4] "standard vs merged" arm)
     for variant in ("pcg", "cg"):
         one_s = S.solve(variant, op1, b, minv=op1.compute_diagonal() if variant == "pcg" else None, config=cfg)
