@@ -265,6 +265,7 @@ def run_slabs(args, rank, local_rank, world):
     from paper_2205_08909_b200 import _lib, dofs, mesh as pmesh, slabs
     from paper_2205_08909_b200.operator import MatrixFreeOperator, OperatorSpec
     from paper_2205_08909_b200.solvers import SolverConfig
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # stdout carries the one JSON line only
     dist.init_process_group("nccl", rank=rank, world_size=world)
     p = args.degree
     cells = workload_cells(args, world)

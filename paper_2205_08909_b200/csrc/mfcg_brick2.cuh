@@ -65,7 +65,7 @@ template <int ID, int COUNT> __device__ __forceinline__ void named_arrive() {
                         // stores, 4 no update at all, 8 no gather, 16 no z sweep, 32 no plane sweeps
 #endif
 #ifndef MFCG_B2_NT
-#define MFCG_B2_NT 5   // transient plane slots (p, v, x)
+#define MFCG_B2_NT 4   // transient plane slots (p, v, x)
 #endif
 #ifndef MFCG_B2_RLAYERS
 #define MFCG_B2_RLAYERS 3  // layers of lattice planes in the ring: the update runs RLAYERS - 1 layers ahead of the gather
@@ -77,7 +77,8 @@ template <int ID, int COUNT> __device__ __forceinline__ void named_arrive() {
 #define MFCG_B2_UNRX 1
 #endif
 #ifndef MFCG_B2_NRL
-#define MFCG_B2_NRL 3  // layers of r' staged on chip
+#define MFCG_B2_NRL 4  // layers of r' staged on chip (3 ring layers, 4 slots, 4 staged layers: best of the combinations
+                       // that fit 227 KB, profiles/r02_notes.md)
 #endif
 
 #ifdef MFCG_TIMING

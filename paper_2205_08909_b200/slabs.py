@@ -154,7 +154,7 @@ class SlabGroup:
         limit = cfg.fixed_iterations or cfg.max_iterations
         args = (_lib.SolveArgs * n)()
         res = (_lib.SolveResultC * n)()
-        keep, hists, outs = [], [], []
+        keep, hists, xouts = [], [], []
         for g, op in enumerate(self.ops):
             a = args[g]
             if location == 0:
@@ -166,10 +166,10 @@ class SlabGroup:
                     raise ValueError("output array must be contiguous float64 of the operator's length")
                 keep.append(b)
                 a.b, a.x = b.ctypes.data, x.ctypes.data
-                outs.append(x)
+                xouts.append(x)
             else:
                 a.b, a.x = int(bs[g]), int(xs[g])
-                outs.append(None)
+                xouts.append(None)
             a.inv_diag = None
             if minvs is not None:
                 if location != 0:
@@ -200,7 +200,7 @@ class SlabGroup:
             k = res[g].iterations
             history = [{"k": i + 1, "alpha": float(hists[g][i, 0]), "beta": float(hists[g][i, 1]),
                         "gamma": float(hists[g][i, 2]), "residual": float(hists[g][i, 3])} for i in range(k)]
-            out.append(SolveResult(outs[g], k, float(res[g].residual), bool(res[g].converged), variant, history,
+            out.append(SolveResult(xouts[g], k, float(res[g].residual), bool(res[g].converged), variant, history,
                                    {"iteration": res[g].solve_ms * 1e-3}, res[g].matvecs, (),
                                    {"solve_ms": res[g].solve_ms, "kernel_launches": res[g].kernel_launches,
                                     "operator_launches": res[g].operator_launches, "bnorm": res[g].bnorm}))
