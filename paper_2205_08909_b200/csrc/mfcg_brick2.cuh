@@ -73,6 +73,9 @@ template <int ID, int COUNT> __device__ __forceinline__ void named_arrive() {
 #ifndef MFCG_B2_UNR
 #define MFCG_B2_UNR 2
 #endif
+#ifndef MFCG_B2_LOOPUNR
+#define MFCG_B2_LOOPUNR 1  // unroll of the update loop over granule pairs
+#endif
 #ifndef MFCG_B2_UNRX
 #define MFCG_B2_UNRX 1
 #endif
@@ -442,7 +445,8 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
               Vec* Xg = reinterpret_cast<Vec*>(X + (e0 - off));
               const unsigned short* it0 = itab - off;
               constexpr int UNR = XM ? MFCG_B2_UNRX : MFCG_B2_UNR;
-#pragma unroll 1
+              constexpr int LOOPUNR = MFCG_B2_LOOPUNR;
+#pragma unroll LOOPUNR
               for (int g0 = g_lo + lane; g0 < g_hi; g0 += UNR * 32) {
                 Vec rr[UNR], vv[UNR], pq[UNR], xx[UNR];
                 unsigned tt[UNR][PER16];
