@@ -52,6 +52,7 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 __device__ __forceinline__ void pin_value(double& v) { asm volatile("" : "+d"(v)); }
 __device__ __forceinline__ void pin_value(float& v) { asm volatile("" : "+f"(v)); }
 __device__ __forceinline__ void pin_value(unsigned& v) { asm volatile("" : "+r"(v)); }
+template <class U> __device__ __forceinline__ void pin_value(U*& v) { asm volatile("" : "+l"(v)); }
 template <int ID, int COUNT> __device__ __forceinline__ void named_barrier() {
   asm volatile("barrier.sync %0, %1;" ::"n"(ID), "n"(COUNT) : "memory");  // non-aligned: lanes of a warp may arrive from different places
 }
@@ -72,6 +73,12 @@ template <int ID, int COUNT> __device__ __forceinline__ void named_arrive() {
 #endif
 #ifndef MFCG_B2_UNR
 #define MFCG_B2_UNR 2
+#endif
+#ifndef MFCG_B2_REGTAB
+#define MFCG_B2_REGTAB 1  // update warps keep their granules' table entries in registers (fp64, shared planes)
+#endif
+#ifndef MFCG_B2_COOP
+#define MFCG_B2_COOP 1  // all update warps share every plane
 #endif
 #ifndef MFCG_B2_LOOPUNR
 #define MFCG_B2_LOOPUNR 1  // unroll of the update loop over granule pairs
@@ -199,7 +206,7 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
   const int xmode = st->xmode;
 
   if (tid == 0) {
-    for (int i = 0; i < NT; ++i) { mbar_init(&H.tfull[i], 1); mbar_init(&H.tupd[i], 32); H.sdone[i] = -1; }
+    for (int i = 0; i < NT; ++i) { mbar_init(&H.tfull[i], 1); mbar_init(&H.tupd[i], MFCG_B2_COOP ? NUPD : 32); H.sdone[i] = -1; }
     for (int i = 0; i < 4; ++i) mbar_init(&H.lfull[i], NUPD);
     for (int i = 0; i < 4; ++i) mbar_init(&H.ldone[i], NLM);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -303,14 +310,7 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
         for (int K = 1; K <= nplanes; ++K) {
           const int q = q_base + K - 1, slot = q % NT;
           B2_TIC(tp);
-          if (q >= NT) mbar_wait(&H.tupd[slot], ((q - NT) / NT) & 1);  // the slot's previous plane has been read
-#ifdef MFCG_B2_EXP_AHEAD
-          if (q >= MFCG_B2_EXP_AHEAD) mbar_wait(&H.tupd[(q - MFCG_B2_EXP_AHEAD) % NT], ((q - MFCG_B2_EXP_AHEAD) / NT) & 1);
-#endif
-          B2_TOC(tp, 0);
           const int gf = g_base + K / P;  // layer whose gather finishes the plane
-          if ((K % P == 0 || K == 1) && gf >= NRL) mbar_wait(&H.ldone[(gf - NRL) & 3], ((gf - NRL) >> 2) & 1);
-          B2_TOC(tp, 1);
           const i64 e0 = st_int + (i64)(K - 1) * nint2d;
           const i64 a0 = e0 & ~(i64)(PER16 - 1);
           const int off = (int)(e0 - a0);
@@ -321,11 +321,20 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
           T* Pb = Tbuf + (slot * 3 + 0) * PLB;
           T* Vb = Tbuf + (slot * 3 + 1) * PLB;
           T* Xb = Tbuf + (slot * 3 + 2) * PLB;
-          mbar_expect_tx(&H.tfull[slot], bytes * (xmode ? 4u : 3u));
-          bulk_g2s(Rb, R + a0, bytes, &H.tfull[slot]);
-          bulk_g2s(Pb, Pv + a0, bytes, &H.tfull[slot]);
-          bulk_g2s(Vb, V + a0, bytes, &H.tfull[slot]);
-          if (xmode) bulk_g2s(Xb, X + a0, bytes, &H.tfull[slot]);
+          const T* Rs = R + a0; const T* Ps = Pv + a0; const T* Vs = V + a0; const T* Xs = X + a0;
+          const unsigned tx = bytes * (xmode ? 4u : 3u);
+          pin_value(Rb); pin_value(Pb); pin_value(Vb); pin_value(Xb);
+          pin_value(Rs); pin_value(Ps); pin_value(Vs); pin_value(Xs);  // addresses are ready before the waits
+          B2_TOC(tp, 2);
+          if (q >= NT) mbar_wait(&H.tupd[slot], ((q - NT) / NT) & 1);  // the slot's previous plane has been read
+          B2_TOC(tp, 0);
+          if ((K % P == 0 || K == 1) && gf >= NRL) mbar_wait(&H.ldone[(gf - NRL) & 3], ((gf - NRL) >> 2) & 1);
+          B2_TOC(tp, 1);
+          mbar_expect_tx(&H.tfull[slot], tx);
+          bulk_g2s(Rb, Rs, bytes, &H.tfull[slot]);
+          bulk_g2s(Pb, Ps, bytes, &H.tfull[slot]);
+          bulk_g2s(Vb, Vs, bytes, &H.tfull[slot]);
+          if (xmode) bulk_g2s(Xb, Xs, bytes, &H.tfull[slot]);
           B2_TOC(tp, 2);
         }
       }
@@ -338,51 +347,30 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
       if (ut < 27) s27[ut] = entity(ut);
       named_barrier<2, NUPD>();
       const i64 st_int = s27[13];
-      const int nperim = fp - nint2d;
-      const int n_in_c = bcx * (P - 1) * bcy * (P - 1);
-      // this thread's brick-boundary position of a lattice plane (the same for every plane of the brick)
-      int pe2 = 0, pcw = 0, po2 = 0, ppstride = 0;
-      if (ut < nperim) {
-        const uint2 d = gtab[n_in_c + ut];
-        pe2 = (int)((d.x >> 19) & 15u); pcw = (int)(d.y & 1023u); po2 = (int)((d.y >> 10) & 4095u);
-        const unsigned sel = d.y >> 22;
-        ppstride = ((sel & 1u) ? Lx - 1 : 1) * ((sel & 2u) ? Ly - 1 : 1);
-      }
-      const i64 pbase1 = s27[pe2 + 9] + po2 - ppstride;  // planes 0 < K < Lz: pbase1 + ppstride * K
-      const bool bnd_xy = mx == 0 || mx == g.mb[0] - 1 || my == 0 || my == g.mb[1] - 1;
       double ls0 = 0.0, ls4 = 0.0;  // r.r and r.Mr of this thread over the brick
+      // A thread meets the same (at most two) granules of every plane of the brick, shifted by the plane's
+      // alignment `off`: their ring offsets and 1/diag classes (itab) stay in registers, so the plane loop has
+      // no dependent table load in front of the 1/diag lookup.  tcache[off][round] = entries of the two elements.
+      constexpr bool CACHED = MFCG_B2_COOP && MFCG_B2_REGTAB && PER16 == 2 &&
+                              ((P * G2::BX - 1) * (P * G2::BY - 1) + 2) / 2 + 1 <= 2 * NUPD;
+      unsigned tcache[2][2] = {{0u, 0u}, {0u, 0u}};
+      if (CACHED) {
+#pragma unroll
+        for (int par = 0; par < 2; ++par)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const int e = (par + ut + c * NUPD) * 2 - par;
+            const unsigned lo = e < nint2d ? itab[e] : 0u, hi = e + 1 < nint2d ? itab[e + 1] : 0u;
+            tcache[par][c] = lo | (hi << 16);
+          }
+      }
       for (int L = 0; L < bcz; ++L) {
         const int gl = g_base + L;
         B2_TIC(tu);
         // the ring planes this layer overwrites were last read by the gather three layers back
         if (gl >= G2::RLAYERS) mbar_wait(&H.ldone[(gl - G2::RLAYERS) & 3], ((gl - G2::RLAYERS) >> 2) & 1);
         B2_TOC(tu, 0);
-                // (b) brick-boundary points of the layer's planes (pre-updated by k_pre): issue the loads now,
-        //     consume them after the interior planes
-        const int k0 = L == 0 ? 0 : 1;
-        unsigned pmk[P + 1];  // mask bytes of this thread's perimeter position, consumed after the planes
-#pragma unroll
-        for (int kk = 0; kk < P + 1; ++kk) pmk[kk] = 0;
-        // Dirichlet DoFs lie on the domain boundary (enforced at operator creation): only bricks that touch it
-        // need the mask bytes
-        const bool need_mask = bnd_xy || (mz == 0 && L == 0) || (mz == g.mb[2] - 1 && L == bcz - 1);
-        if (ut < nperim) {
-          const int nk = P + 1 - k0;
-#pragma unroll
-          for (int kk = 0; kk < P + 1; ++kk) {
-            if (kk >= nk) break;
-            const int K = L * P + k0 + kk;
-            const int ez = K == 0 ? 0 : (K == Lz ? 2 : 1);
-            const i64 gi = ez == 1 ? pbase1 + (i64)ppstride * K : s27[pe2 + 9 * ez] + po2;
-            MFCG_CHECK(gi >= n_int && gi < g.n_dofs && pcw < PLANE && K <= Lz);
-            const int dst = ((kb_base + K) % RB) * PLANE + pcw;
-            // asynchronous copy straight into the ring (LDGSTS); constrained points are zeroed afterwards
-            asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(ring + dst)), "l"(Pv + gi),
-                         "n"((int)sizeof(T)) : "memory");
-            if (need_mask) pmk[kk] = g.mask[gi - n_int];
-          }
-        }
-        B2_TOC(tu, 3);
+        // (the brick-boundary values of the layer's planes are fetched by the plane-sweep warps)
         // (a) interior planes: pre update in place in the staged planes (solvers.py:660-690)
         const int Kfirst = L == 0 ? 1 : L * P + 1;
         const int Klast = L * P + P < Lz - 1 ? L * P + P : Lz - 1;
@@ -392,7 +380,7 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
 #ifdef MFCG_B2_EXP_SYNC
             if (q % (NUPD / 32) == uw) {
 #else
-            if (q % (NUPD / 32) != uw) continue;  // whole planes round-robin over the update warps
+            if (!MFCG_B2_COOP && q % (NUPD / 32) != uw) continue;  // whole planes round-robin over the update warps
 #endif
             const int gf = g_base + K / P;
             T* Rb = Rbuf + ((gf % NRL) * P + K % P) * PLB;
@@ -413,7 +401,7 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
             // parity of the phase before that would let the wait below through (seen as wrong results / hangs
             // once in a few hundred launches on ragged brick grids with NT = 5).  The warp that consumed the
             // slot's previous plane publishes its number; once that is visible the barrier is in our phase.
-            if (q >= NT) {
+            if (!MFCG_B2_COOP && q >= NT) {
               const volatile int* sd = H.sdone + slot;
               while (*sd < q - NT) {}
             }
@@ -424,6 +412,10 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
             // checks.  The (at most two) partial granules at the ends go element by element.
             const int g_lo = off ? 1 : 0, g_hi = (off + tail0) / PER16;
             const int lane = ut & 31;
+            // all four warps work on every plane (a transient slot is then held for a quarter of the time), or
+            // whole planes round-robin over the warps
+            constexpr int GSTR = MFCG_B2_COOP ? NUPD : 32;
+            const int gl0 = MFCG_B2_COOP ? ut : lane;
             auto update_plane = [&](auto xm_) {
               constexpr int XM = decltype(xm_)::value;
               struct alignas(16) Vec { T v[PER16]; };
@@ -446,25 +438,39 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
               const unsigned short* it0 = itab - off;
               constexpr int UNR = XM ? MFCG_B2_UNRX : MFCG_B2_UNR;
               constexpr int LOOPUNR = MFCG_B2_LOOPUNR;
+              int round = 0;
 #pragma unroll LOOPUNR
-              for (int g0 = g_lo + lane; g0 < g_hi; g0 += UNR * 32) {
+              for (int g0 = g_lo + gl0; g0 < g_hi; g0 += UNR * GSTR, round += UNR) {
                 Vec rr[UNR], vv[UNR], pq[UNR], xx[UNR];
                 unsigned tt[UNR][PER16];
+                T mm[UNR][PER16];
+                // warp-uniform: some lane of this warp has a granule in the next round
+                const bool more = g0 - lane + GSTR < g_hi;
 #pragma unroll
                 for (int c = 0; c < UNR; ++c) {
-                  const int gq = g0 + c * 32 < g_hi ? g0 + c * 32 : g0;  // the tail repeats granule g0 (discarded)
+                  if (c > 0 && !more) break;
+                  const int gq = g0 + c * GSTR < g_hi ? g0 + c * GSTR : g0;  // the tail repeats granule g0 (discarded)
                   rr[c] = Rv[gq]; vv[c] = Vv[gq]; pq[c] = Pq[gq];
                   if (XM) xx[c] = Xv[gq];
+                  if (CACHED) {
+                    const int j = UNR == 2 ? c : round;  // planes have at most two rounds here
+                    const unsigned pk = off ? (j ? tcache[1][1] : tcache[1][0]) : (j ? tcache[0][1] : tcache[0][0]);
+                    tt[c][0] = pk & 0xffffu;
+                    tt[c][PER16 - 1] = pk >> 16;
+                  } else {
 #pragma unroll
-                  for (int w = 0; w < PER16; ++w) tt[c][w] = (MFCG_B2_SKIP & 64) ? 0u : it0[gq * PER16 + w];
+                    for (int w = 0; w < PER16; ++w) tt[c][w] = (MFCG_B2_SKIP & 64) ? 0u : it0[gq * PER16 + w];
+                  }
+#pragma unroll
+                  for (int w = 0; w < PER16; ++w) mm[c][w] = (MFCG_B2_SKIP & 64) ? (T)1 : dcls[tt[c][w] >> 10];
                 }
 #pragma unroll
                 for (int c = 0; c < UNR; ++c) {
-                  const int gq = g0 + c * 32;
+                  const int gq = g0 + c * GSTR;
                   if (c > 0 && gq >= g_hi) break;
 #pragma unroll
                   for (int w = 0; w < PER16; ++w) {
-                    const T m = (MFCG_B2_SKIP & 64) ? (T)1 : dcls[tt[c][w] >> 10];
+                    const T m = mm[c][w];
                     T xdummy = (T)0;
                     pre(rr[c].v[w], pq[c].v[w], XM ? xx[c].v[w] : xdummy, vv[c].v[w], m);
                     MFCG_CHECK((int)(tt[c][w] & 1023u) < PLANE);
@@ -480,7 +486,7 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
               }
               // partial granules: element e of the head [0, head) or the tail [tail0, nint2d)
               const int npart = head + (nint2d - tail0);
-              if (lane < npart) {
+              if (lane < npart && (!MFCG_B2_COOP || uw == NUPD / 32 - 1)) {
                 const int e = lane < head ? lane : tail0 + (lane - head);
                 const unsigned t = itab[e];
                 const T m = dcls[t >> 10];
@@ -498,7 +504,7 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
             else if (xmode == 0) update_plane(std::integral_constant<int, 0>());
             else if (xmode == 1) update_plane(std::integral_constant<int, 1>());
             else update_plane(std::integral_constant<int, 2>());
-            if (lane == 0) *(volatile int*)(H.sdone + slot) = q;
+            if (!MFCG_B2_COOP && lane == 0) *(volatile int*)(H.sdone + slot) = q;
             mbar_arrive(&H.tupd[slot]);  // the transient slot (p, v, x) has been read
 #ifdef MFCG_B2_EXP_SYNC
             }
@@ -507,34 +513,6 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
 #endif
             B2_TOC(tu, 2);
           }
-        B2_TOC(tu, 5);
-        asm volatile("cp.async.wait_all;" ::: "memory");
-#pragma unroll
-        for (int kk = 0; kk < P + 1; ++kk) {
-          pin_value(pmk[kk]);  // keeps the loads in flight until here
-          // constrained entries enter the operator as 0 (operator.py:341-342)
-          if (pmk[kk] & 1u) ring[((kb_base + L * P + k0 + kk) % RB) * PLANE + pcw] = (T)0;
-        }
-        // (c) the brick's bottom / top face interiors (first / last layer only): contiguous
-#pragma unroll
-        for (int side = 0; side < 2; ++side) {
-          if (side == 0 ? (L != 0) : (L != bcz - 1)) continue;
-          const i64 fb = s27[side == 0 ? 4 : 22];
-          T* pl = ring + ((kb_base + (side == 0 ? 0 : Lz)) % RB) * PLANE;
-          unsigned fbits = 0;
-          int cnt = 0;
-          const bool face_mask = side == 0 ? mz == 0 : mz == g.mb[2] - 1;  // the face lies on the domain boundary
-          for (int it = ut; it < nint2d; it += NUPD, ++cnt) {
-            MFCG_CHECK(fb + it >= n_int && fb + it < g.n_dofs);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(pl + (itab[it] & 1023u))),
-                         "l"(Pv + fb + it), "n"((int)sizeof(T)) : "memory");
-            if (face_mask) fbits |= (unsigned)(g.mask[fb + it - n_int] & 1) << cnt;
-          }
-          asm volatile("cp.async.wait_all;" ::: "memory");
-          cnt = 0;
-          for (int it = ut; it < nint2d; it += NUPD, ++cnt)
-            if (fbits & (1u << cnt)) pl[itab[it] & 1023u] = (T)0;
-        }
         B2_TOC(tu, 4);
         if (L == bcz - 1) {  // handed over with the brick's last layer
 #pragma unroll
@@ -549,10 +527,100 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
       }
     } else if constexpr (ROLE == 0) {
       // ================================ plane sweeps (warpgroup 0) ================================
+      // Brick-boundary values of p' (pre-updated by k_pre, unchanged during this launch) go straight into the
+      // ring with 8-byte cp.async, one layer ahead of the sweeps: these warps idle while the update warps work.
+      i64* s27 = H.st27[1];
+      named_barrier<6, NS1>();
+      if (tid < 27) s27[tid] = entity(tid);
+      named_barrier<6, NS1>();
+      const int nperim = fp - nint2d;
+      const int n_in_c = bcx * (P - 1) * bcy * (P - 1);
+      // this thread's brick-boundary position of a lattice plane (the same for every plane of the brick)
+      int pe2 = 0, pcw = 0, po2 = 0, ppstride = 0;
+      if (tid < nperim) {
+        const uint2 d = gtab[n_in_c + tid];
+        pe2 = (int)((d.x >> 19) & 15u); pcw = (int)(d.y & 1023u); po2 = (int)((d.y >> 10) & 4095u);
+        const unsigned sel = d.y >> 22;
+        ppstride = ((sel & 1u) ? Lx - 1 : 1) * ((sel & 2u) ? Ly - 1 : 1);
+      }
+      const i64 pbase1 = s27[pe2 + 9] + po2 - ppstride;  // planes 0 < K < Lz: pbase1 + ppstride * K
+      const bool bnd_xy = mx == 0 || mx == g.mb[0] - 1 || my == 0 || my == g.mb[1] - 1;
+      // ZERO = false: issue the copies of layer L, return the Dirichlet bits of this thread's values
+      // (bits 0..P: planes, 8.., 16..: bottom / top face); ZERO = true: zero the flagged values (operator.py:341-342)
+      auto boundary = [&](int L, auto zero_c, unsigned bits) -> unsigned {
+        constexpr bool ZERO = decltype(zero_c)::value;
+        const int k0 = L == 0 ? 0 : 1;
+        // Dirichlet DoFs lie on the domain boundary (enforced at operator creation): only bricks that touch it
+        // need the mask bytes
+        const bool need_mask = bnd_xy || (mz == 0 && L == 0) || (mz == g.mb[2] - 1 && L == bcz - 1);
+        unsigned out = 0;
+        if (tid < nperim) {
+          const int nk = P + 1 - k0;
+#pragma unroll
+          for (int kk = 0; kk < P + 1; ++kk) {
+            if (kk >= nk) break;
+            const int K = L * P + k0 + kk;
+            const int dst = ((kb_base + K) % RB) * PLANE + pcw;
+            if (ZERO) {
+              if (bits & (1u << kk)) ring[dst] = (T)0;
+              continue;
+            }
+            const int ez = K == 0 ? 0 : (K == Lz ? 2 : 1);
+            const i64 gi = ez == 1 ? pbase1 + (i64)ppstride * K : s27[pe2 + 9 * ez] + po2;
+            MFCG_CHECK(gi >= n_int && gi < g.n_dofs && pcw < PLANE && K <= Lz);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(ring + dst)), "l"(Pv + gi),
+                         "n"((int)sizeof(T)) : "memory");
+            if (need_mask) out |= (unsigned)(g.mask[gi - n_int] & 1) << kk;
+          }
+        }
+        // the brick's bottom / top face interiors (first / last layer only): contiguous in memory
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+          if (side == 0 ? (L != 0) : (L != bcz - 1)) continue;
+          const i64 fb = s27[side == 0 ? 4 : 22];
+          T* pl = ring + ((kb_base + (side == 0 ? 0 : Lz)) % RB) * PLANE;
+          const bool face_mask = side == 0 ? mz == 0 : mz == g.mb[2] - 1;  // the face lies on the domain boundary
+          int cnt = 8 + 8 * side;
+          for (int it = tid; it < nint2d; it += NS1, ++cnt) {
+            T* dstp = pl + (itab[it] & 1023u);
+            if (ZERO) {
+              if (bits & (1u << cnt)) *dstp = (T)0;
+              continue;
+            }
+            MFCG_CHECK(fb + it >= n_int && fb + it < g.n_dofs);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(dstp)), "l"(Pv + fb + it),
+                         "n"((int)sizeof(T)) : "memory");
+            if (face_mask) out |= (unsigned)(g.mask[fb + it - n_int] & 1) << cnt;
+          }
+        }
+        if (!ZERO) asm volatile("cp.async.commit_group;" ::: "memory");
+        return out;
+      };
+      static_assert((P * G2::BX + 1) * 2 + (P * G2::BY - 1) * 2 <= NS1, "one brick-boundary position per thread");
+      static_assert(((P * G2::BX - 1) * (P * G2::BY - 1) + NS1 - 1) / NS1 <= 8, "face bits");
+      // the ring planes a layer overwrites were last read by the gather RLAYERS layers back; that gather had
+      // finished before these warps were let into the layer before this one (tile barrier), so no wait is needed
+      // beyond the check below (immediate)
+      auto ring_free = [&](int gq) {
+        if (gq >= G2::RLAYERS) mbar_wait(&H.ldone[(gq - G2::RLAYERS) & 3], ((gq - G2::RLAYERS) >> 2) & 1);
+      };
+      ring_free(g_base);
+      unsigned bits_cur = boundary(0, std::false_type(), 0u), bits_next = 0;
       for (int L = 0; L < bcz; ++L) {
         const int gl = g_base + L;
         const int sl0 = (kb_base + L * P) % RB;
         B2_TIC(tm);
+        if (L + 1 < bcz) {
+          ring_free(gl + 1);
+          bits_next = boundary(L + 1, std::false_type(), 0u);
+          asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+          asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        if (bits_cur) boundary(L, std::true_type(), bits_cur);
+        bits_cur = bits_next;
+        named_barrier<6, NS1>();  // every thread's values of layer L have landed
+        B2_TOC(tm, 4);
         mbar_wait(&H.lfull[gl & 3], (gl >> 2) & 1);
         B2_TOC(tm, 0);
         // ---- stage 1: thread = (cell, z plane k); the plane goes to registers, x and y sweeps there:
@@ -787,6 +855,7 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
   if (tid == 0 || tid == T_LM || tid == T_PROD || tid == T_UPD)
     for (int i = 0; i < (tid == T_UPD ? 6 : 4); ++i)
       atomicAdd(&g_phase_cycles[(tid == 0 ? 0 : (tid == T_LM ? 4 : (tid == T_PROD ? 8 : 12))) + i], tacc[i]);
+  if (tid == 0) atomicAdd(&g_phase_cycles[18], tacc[4]);  // plane-sweep warps: brick-boundary fetch
 #endif
   };
   // register re-allocation between the warpgroups: the plane sweeps hold 2 (p+1)^2 values per thread
