@@ -547,7 +547,7 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
       const bool bnd_xy = mx == 0 || mx == g.mb[0] - 1 || my == 0 || my == g.mb[1] - 1;
       // ZERO = false: issue the copies of layer L, return the Dirichlet bits of this thread's values
       // (bits 0..P: planes, 8.., 16..: bottom / top face); ZERO = true: zero the flagged values (operator.py:341-342)
-      auto boundary = [&](int L, auto zero_c, unsigned bits) -> unsigned {
+      auto boundary = [&](int L, auto zero_c, unsigned bits, unsigned (&pm)[P + 1]) -> unsigned {
         constexpr bool ZERO = decltype(zero_c)::value;
         const int k0 = L == 0 ? 0 : 1;
         // Dirichlet DoFs lie on the domain boundary (enforced at operator creation): only bricks that touch it
@@ -568,9 +568,14 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
             const int ez = K == 0 ? 0 : (K == Lz ? 2 : 1);
             const i64 gi = ez == 1 ? pbase1 + (i64)ppstride * K : s27[pe2 + 9 * ez] + po2;
             MFCG_CHECK(gi >= n_int && gi < g.n_dofs && pcw < PLANE && K <= Lz);
+#ifndef MFCG_B2_EXP_NOCP
             asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(ring + dst)), "l"(Pv + gi),
                          "n"((int)sizeof(T)) : "memory");
-            if (need_mask) out |= (unsigned)(g.mask[gi - n_int] & 1) << kk;
+#else
+            if (gi == -12345) ring[dst] = (T)0;
+#endif
+            // the mask byte stays an outstanding load: it is folded into the flag bits after this layer's sweeps
+            if (need_mask) pm[kk] = g.mask[gi - n_int];
           }
         }
         // the brick's bottom / top face interiors (first / last layer only): contiguous in memory
@@ -604,21 +609,32 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
       auto ring_free = [&](int gq) {
         if (gq >= G2::RLAYERS) mbar_wait(&H.ldone[(gq - G2::RLAYERS) & 3], ((gq - G2::RLAYERS) >> 2) & 1);
       };
+      unsigned pm[P + 1];
+      auto fold = [&](unsigned b) {  // Dirichlet flags of the values issued last
+#pragma unroll
+        for (int kk = 0; kk < P + 1; ++kk) {
+          pin_value(pm[kk]);
+          b |= (pm[kk] & 1u) << kk;
+          pm[kk] = 0u;
+        }
+        return b;
+      };
+#pragma unroll
+      for (int kk = 0; kk < P + 1; ++kk) pm[kk] = 0u;
       ring_free(g_base);
-      unsigned bits_cur = boundary(0, std::false_type(), 0u), bits_next = 0;
+      unsigned bits_cur = fold(boundary(0, std::false_type(), 0u, pm)), bits_next = 0;
       for (int L = 0; L < bcz; ++L) {
         const int gl = g_base + L;
         const int sl0 = (kb_base + L * P) % RB;
         B2_TIC(tm);
         if (L + 1 < bcz) {
           ring_free(gl + 1);
-          bits_next = boundary(L + 1, std::false_type(), 0u);
+          bits_next = boundary(L + 1, std::false_type(), 0u, pm);
           asm volatile("cp.async.wait_group 1;" ::: "memory");
         } else {
           asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
-        if (bits_cur) boundary(L, std::true_type(), bits_cur);
-        bits_cur = bits_next;
+        if (bits_cur) boundary(L, std::true_type(), bits_cur, pm);
         named_barrier<6, NS1>();  // every thread's values of layer L have landed
         B2_TOC(tm, 4);
         mbar_wait(&H.lfull[gl & 3], (gl >> 2) & 1);
@@ -695,6 +711,8 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
         }
         if (!tiles_free && gl > 0) named_barrier<4, NS1 + NLM>();
         named_arrive<3, NS1 + NLM>();  // tiles of layer gl written
+        bits_cur = fold(bits_next);
+        bits_next = 0u;
         B2_TOC(tm, 3);
 
       }
