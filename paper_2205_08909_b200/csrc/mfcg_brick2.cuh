@@ -277,7 +277,7 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
   int g_base = 0, q_base = 0;  // running layer / plane counters of this block (the barrier phases follow them)
   int kb_base = 0;             // running lattice-plane counter: ring slot of plane K of a brick = (kb_base + K) % RB
 #ifdef MFCG_TIMING
-  unsigned long long tacc[6] = {0, 0, 0, 0, 0, 0};
+  unsigned long long tacc[6] = {0, 0, 0, 0, 0, 0}, tacc6 = 0;
 #endif
   for (int bi = blockIdx.x; bi < brick_count; bi += gridDim.x) {
     const int b = brick_first + bi;
@@ -543,7 +543,8 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
         const unsigned sel = d.y >> 22;
         ppstride = ((sel & 1u) ? Lx - 1 : 1) * ((sel & 2u) ? Ly - 1 : 1);
       }
-      const i64 pbase1 = s27[pe2 + 9] + po2 - ppstride;  // planes 0 < K < Lz: pbase1 + ppstride * K
+      const T* src1 = Pv + (s27[pe2 + 9] + po2 - ppstride);  // planes 0 < K < Lz: src1[ppstride * K]
+      const unsigned ring_pos = smem_u32(ring + pcw);
       const bool bnd_xy = mx == 0 || mx == g.mb[0] - 1 || my == 0 || my == g.mb[1] - 1;
       // ZERO = false: issue the copies of layer L, return the Dirichlet bits of this thread's values
       // (bits 0..P: planes, 8.., 16..: bottom / top face); ZERO = true: zero the flagged values (operator.py:341-342)
@@ -556,26 +557,23 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
         unsigned out = 0;
         if (tid < nperim) {
           const int nk = P + 1 - k0;
+          int K = L * P + k0;
+          int slot = (kb_base + K) % RB;
+          const T* src = src1 + (i64)ppstride * K;  // planes strictly inside the brick: one stride apart
 #pragma unroll
-          for (int kk = 0; kk < P + 1; ++kk) {
+          for (int kk = 0; kk < P + 1; ++kk, ++K, src += ppstride, slot = slot + 1 == RB ? 0 : slot + 1) {
             if (kk >= nk) break;
-            const int K = L * P + k0 + kk;
-            const int dst = ((kb_base + K) % RB) * PLANE + pcw;
             if (ZERO) {
-              if (bits & (1u << kk)) ring[dst] = (T)0;
+              if (bits & (1u << kk)) ring[slot * PLANE + pcw] = (T)0;
               continue;
             }
-            const int ez = K == 0 ? 0 : (K == Lz ? 2 : 1);
-            const i64 gi = ez == 1 ? pbase1 + (i64)ppstride * K : s27[pe2 + 9 * ez] + po2;
-            MFCG_CHECK(gi >= n_int && gi < g.n_dofs && pcw < PLANE && K <= Lz);
-#ifndef MFCG_B2_EXP_NOCP
-            asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(ring + dst)), "l"(Pv + gi),
-                         "n"((int)sizeof(T)) : "memory");
-#else
-            if (gi == -12345) ring[dst] = (T)0;
-#endif
+            const T* sp = src;
+            if (K == 0 || K == Lz) sp = Pv + s27[pe2 + (K == 0 ? 0 : 18)] + po2;  // the brick's bottom / top plane
+            MFCG_CHECK(sp - Pv >= n_int && sp - Pv < g.n_dofs && pcw < PLANE && K <= Lz);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(ring_pos + (unsigned)(slot * PLANE * (int)sizeof(T))),
+                         "l"(sp), "n"((int)sizeof(T)) : "memory");
             // the mask byte stays an outstanding load: it is folded into the flag bits after this layer's sweeps
-            if (need_mask) pm[kk] = g.mask[gi - n_int];
+            if (need_mask) pm[kk] = g.mask[(sp - Pv) - n_int];
           }
         }
         // the brick's bottom / top face interiors (first / last layer only): contiguous in memory
@@ -629,14 +627,20 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
         B2_TIC(tm);
         if (L + 1 < bcz) {
           ring_free(gl + 1);
+          B2_TOC(tm, 5);
           bits_next = boundary(L + 1, std::false_type(), 0u, pm);
+          B2_TOC(tm, 4);
           asm volatile("cp.async.wait_group 1;" ::: "memory");
         } else {
           asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
         if (bits_cur) boundary(L, std::true_type(), bits_cur, pm);
+        B2_TOC(tm, 5);
         named_barrier<6, NS1>();  // every thread's values of layer L have landed
-        B2_TOC(tm, 4);
+#ifdef MFCG_TIMING
+        { volatile double* vv_ = &H.bsum[0]; (void)*vv_; }  // the barrier blocks at the first dependent access
+        { long long n__ = clock64(); tacc6 += (unsigned long long)(n__ - tm); tm = n__; }
+#endif
         mbar_wait(&H.lfull[gl & 3], (gl >> 2) & 1);
         B2_TOC(tm, 0);
         // ---- stage 1: thread = (cell, z plane k); the plane goes to registers, x and y sweeps there:
@@ -873,7 +877,11 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
   if (tid == 0 || tid == T_LM || tid == T_PROD || tid == T_UPD)
     for (int i = 0; i < (tid == T_UPD ? 6 : 4); ++i)
       atomicAdd(&g_phase_cycles[(tid == 0 ? 0 : (tid == T_LM ? 4 : (tid == T_PROD ? 8 : 12))) + i], tacc[i]);
-  if (tid == 0) atomicAdd(&g_phase_cycles[18], tacc[4]);  // plane-sweep warps: brick-boundary fetch
+  if (tid == 0) {  // plane-sweep warps, brick-boundary fetch: issue, ring check + landing + zeroing, barrier
+    atomicAdd(&g_phase_cycles[18], tacc[4]);
+    atomicAdd(&g_phase_cycles[19], tacc[5]);
+    atomicAdd(&g_phase_cycles[20], tacc6);
+  }
 #endif
   };
   // register re-allocation between the warpgroups: the plane sweeps hold 2 (p+1)^2 values per thread
