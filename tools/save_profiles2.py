@@ -76,9 +76,9 @@ stalls = [k for k in hdr if k.startswith('stall_') and 'Not Issued' not in k]
 agg2 = {m[0]: Counter() for m in marks[:-1]}
 cur = 0
 for r in lines2:
-    try:
-        if r[0].strip(): cur = int(r[0])
-    except ValueError: pass
+    if not r[0].strip(): continue  # SASS rows repeat what their source row sums up
+    try: cur = int(r[0])
+    except ValueError: continue
     for (name, lo), (_, hi) in zip(marks[:-1], marks[1:]):
         if lo <= cur < hi:
             for s in stalls: agg2[name][s] += f(r, s)
