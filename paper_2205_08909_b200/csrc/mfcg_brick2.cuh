@@ -77,9 +77,6 @@ template <int ID, int COUNT> __device__ __forceinline__ void named_arrive() {
 #ifndef MFCG_B2_REGTAB
 #define MFCG_B2_REGTAB 1  // update warps keep their granules' table entries in registers (fp64, shared planes)
 #endif
-#ifndef MFCG_B2_COOP
-#define MFCG_B2_COOP 1  // all update warps share every plane
-#endif
 #ifndef MFCG_B2_LOOPUNR
 #define MFCG_B2_LOOPUNR 1  // unroll of the update loop over granule pairs
 #endif
@@ -172,7 +169,6 @@ struct Hdr2 {
   unsigned long long lfull[4], ldone[4]; // layer ready for the math warps / gather of a layer finished
   double lsum[4][8][2];                  // r.r and r.Mr of a layer, per update warp
   double bsum[2];                        // their running sums over the brick
-  int sdone[8];                          // last plane consumed from a transient slot
   double red[8][8];
 };
 static_assert(sizeof(Hdr2) <= 2048, "header");
@@ -206,7 +202,7 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
   const int xmode = st->xmode;
 
   if (tid == 0) {
-    for (int i = 0; i < NT; ++i) { mbar_init(&H.tfull[i], 1); mbar_init(&H.tupd[i], MFCG_B2_COOP ? NUPD : 32); H.sdone[i] = -1; }
+    for (int i = 0; i < NT; ++i) { mbar_init(&H.tfull[i], 1); mbar_init(&H.tupd[i], NUPD); }
     for (int i = 0; i < 4; ++i) mbar_init(&H.lfull[i], NUPD);
     for (int i = 0; i < 4; ++i) mbar_init(&H.ldone[i], NLM);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -351,7 +347,7 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
       // A thread meets the same (at most two) granules of every plane of the brick, shifted by the plane's
       // alignment `off`: their ring offsets and 1/diag classes (itab) stay in registers, so the plane loop has
       // no dependent table load in front of the 1/diag lookup.  tcache[off][round] = entries of the two elements.
-      constexpr bool CACHED = MFCG_B2_COOP && MFCG_B2_REGTAB && PER16 == 2 &&
+      constexpr bool CACHED = MFCG_B2_REGTAB && PER16 == 2 &&
                               ((P * G2::BX - 1) * (P * G2::BY - 1) + 2) / 2 + 1 <= 2 * NUPD;
       unsigned tcache[2][2] = {{0u, 0u}, {0u, 0u}};
       if (CACHED) {
@@ -377,11 +373,6 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
         if (nint2d > 0)
           for (int K = Kfirst; K <= Klast; ++K) {
             const int q = q_base + K - 1, slot = q % NT;
-#ifdef MFCG_B2_EXP_SYNC
-            if (q % (NUPD / 32) == uw) {
-#else
-            if (!MFCG_B2_COOP && q % (NUPD / 32) != uw) continue;  // whole planes round-robin over the update warps
-#endif
             const int gf = g_base + K / P;
             T* Rb = Rbuf + ((gf % NRL) * P + K % P) * PLB;
             const T* Pb = Tbuf + (slot * 3 + 0) * PLB;
@@ -396,15 +387,10 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
             if (tail0 < head) tail0 = head;
             const T* dcls = dtab + (K % P) * P * P;
             T* rplane = ring + ((kb_base + K) % RB) * PLANE;
-            // Phase parity only tells "this phase" from "the previous one", and this warp's previous plane sat
-            // in another slot: the slot's previous plane (another warp's) may not even have landed yet, and the
-            // parity of the phase before that would let the wait below through (seen as wrong results / hangs
-            // once in a few hundred launches on ragged brick grids with NT = 5).  The warp that consumed the
-            // slot's previous plane publishes its number; once that is visible the barrier is in our phase.
-            if (!MFCG_B2_COOP && q >= NT) {
-              const volatile int* sd = H.sdone + slot;
-              while (*sd < q - NT) {}
-            }
+            // All four warps take part in every plane, so a warp revisits a transient slot only after its own
+            // arrival on `tupd` for the slot's previous plane: it is never two phases ahead of the barrier (phase
+            // parity only tells "this phase" from "the previous one"; with whole planes per warp this was a race,
+            // profiles/r02_notes.md).
             mbar_wait(&H.tfull[slot], (q / NT) & 1);
             B2_TOC(tu, 1);
             // 16-byte granules of the staged plane (buffer index bi = off + e).  Granules [g_lo, g_hi) lie
@@ -412,10 +398,9 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
             // checks.  The (at most two) partial granules at the ends go element by element.
             const int g_lo = off ? 1 : 0, g_hi = (off + tail0) / PER16;
             const int lane = ut & 31;
-            // all four warps work on every plane (a transient slot is then held for a quarter of the time), or
-            // whole planes round-robin over the warps
-            constexpr int GSTR = MFCG_B2_COOP ? NUPD : 32;
-            const int gl0 = MFCG_B2_COOP ? ut : lane;
+            // all four warps work on every plane: a transient slot is held for a quarter of the time
+            constexpr int GSTR = NUPD;
+            const int gl0 = ut;
             auto update_plane = [&](auto xm_) {
               constexpr int XM = decltype(xm_)::value;
               struct alignas(16) Vec { T v[PER16]; };
@@ -486,7 +471,7 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
               }
               // partial granules: element e of the head [0, head) or the tail [tail0, nint2d)
               const int npart = head + (nint2d - tail0);
-              if (lane < npart && (!MFCG_B2_COOP || uw == NUPD / 32 - 1)) {
+              if (lane < npart && uw == NUPD / 32 - 1) {
                 const int e = lane < head ? lane : tail0 + (lane - head);
                 const unsigned t = itab[e];
                 const T m = dcls[t >> 10];
@@ -504,13 +489,7 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
             else if (xmode == 0) update_plane(std::integral_constant<int, 0>());
             else if (xmode == 1) update_plane(std::integral_constant<int, 1>());
             else update_plane(std::integral_constant<int, 2>());
-            if (!MFCG_B2_COOP && lane == 0) *(volatile int*)(H.sdone + slot) = q;
             mbar_arrive(&H.tupd[slot]);  // the transient slot (p, v, x) has been read
-#ifdef MFCG_B2_EXP_SYNC
-            }
-            named_barrier<2, NUPD>();
-            {
-#endif
             B2_TOC(tu, 2);
           }
         B2_TOC(tu, 4);
