@@ -228,6 +228,7 @@ class Engine : public EngineBase {
       }
     }
     vgrid_ = c_->ctx->sm_count * 8;
+    if (const char* env = std::getenv("MFCG_COMP_INTERLEAVE")) comp_interleave_ = env[0] != '0';
     // one scalar field per component, fields 256-byte aligned; the gaps stay zero
     C_ = c_->ncomp;
     cs_ = C_ == 1 ? c_->grid.n_dofs : (c_->grid.n_dofs + 31) / 32 * 32;
@@ -417,6 +418,18 @@ class Engine : public EngineBase {
     }
     const unsigned nb = (unsigned)count;
     const int off = (int)first;
+    // Several components on stored geometry go out as ONE launch with the blocks of a brick next to each other
+    // (block = brick * C + component): the brick's geometry -- the largest stream of these kernels -- crosses HBM
+    // once and is served from L2 to the other components.  MFCG_COMP_INTERLEAVE=0: one launch per component.
+    if (C_ > 1 && general_ && !cellpath_ && c_->geometry != MFCG_GEOM_QUADRATIC_COMPUTE && comp_interleave_) {
+      const i64 ps = 8 * rows_pc_;
+      if (mode == 0)
+        k_brick<P, T, 0, 1><<<nb * C_, Cfg<P, 1>::THREADS, smem_, stream()>>>(
+            c_->grid, tab_, gen_, geo_, src, nullptr, v, nullptr, nullptr, nullptr, nullptr, nullptr, off, C_, cs_, ps);
+      else
+        k_brick<P, T, 1, 1><<<nb * C_, Cfg<P, 1>::THREADS, smem_, stream()>>>(
+            c_->grid, tab_, gen_, geo_, nullptr, pv, v, r_, x_, minv_, c_->d_state, partials, off, C_, cs_, ps);
+    } else
     for (int comp = 0; comp < C_; ++comp) {
       const i64 o = comp * cs_;
       const T* s_ = src ? src + o : nullptr;
@@ -959,6 +972,7 @@ class Engine : public EngineBase {
   void* geo_a_ = nullptr;
   void* geo_b_ = nullptr;
   i64 geo_bytes_ = 0;
+  bool comp_interleave_ = true;  // several components on stored geometry in one launch
   bool general_ = false;
   bool cellpath_ = false;  // curved mesh with n_q_1d != p+1: cell-by-cell apply
   CellTables ctab_{};

@@ -554,7 +554,8 @@ __global__ void __launch_bounds__(Cfg<P, G>::THREADS, Cfg<P, G>::MINB)
 k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAccess geo,
         const T* __restrict__ src, T* __restrict__ Pv,
         T* __restrict__ V, T* __restrict__ R, T* __restrict__ X, const T* __restrict__ Minv,
-        const SolveState* __restrict__ st, double* __restrict__ partials, int brick_offset) {
+        const SolveState* __restrict__ st, double* __restrict__ partials, int brick_offset,
+        int ncomp = 1, i64 comp_stride = 0, i64 part_stride = 0) {
   constexpr int N = P + 1, RS = Geo<P, G>::RS, PSTR = Geo<P, G>::PSTR, TILE = Geo<P, G>::TILE, WX = Geo<P, G>::WX,
                 PLANE = Geo<P, G>::PLANE, NCELL = Geo<P, G>::NCELL, RB = Geo<P, G>::RB,
                 NT_C = Cfg<P, G>::NT_C, NT_P = Cfg<P, G>::NT_P, KC = Cfg<P, G>::KC, HE = EOShape<N>::HE,
@@ -591,7 +592,22 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
     am1 = (T)st->am1; bm1 = (T)st->bm1; xc1 = (T)st->xc1; xc2 = (T)st->xc2; xmode = st->xmode;
   }
 
-  const int b = blockIdx.x + brick_offset;  // slab runs launch the interface brick layers first
+  // ncomp > 1 (stored geometry, several components in one launch): consecutive blocks work on the same brick, one
+  // component each, so the brick's geometry block comes from HBM once and from L2 for the other components
+  int bidx = blockIdx.x;
+  if (ncomp > 1) {
+    const int comp = bidx % ncomp;
+    bidx /= ncomp;
+    const i64 o = comp * comp_stride;
+    if (src) src += o;
+    if (Pv) Pv += o;
+    V += o;
+    if (R) R += o;
+    if (X) X += o;
+    if (Minv) Minv += o;
+    if (partials) partials += comp * part_stride;
+  }
+  const int b = bidx + brick_offset;  // slab runs launch the interface brick layers first
   const int mx = b % g.mb[0];
   const int my = (b / g.mb[0]) % g.mb[1];
   const int mz = b / (g.mb[0] * g.mb[1]);

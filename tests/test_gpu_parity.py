@@ -354,6 +354,34 @@ def test_three_components_vs_reference(golden, ci):
         S.solve("combined_pcg", op, b, minv=np.ones(h.n_dofs))
 
 
+def test_three_components_curved_one_launch(monkeypatch):
+    """Stored geometry with three components: one launch, the blocks of a brick next to each other so that its
+    geometry is read from HBM once (MFCG_COMP_INTERLEAVE=0: one launch per component).  Same results either way."""
+    S = _solvers()
+    cells, p, nq, amp = (9, 7, 6), 4, 5, 0.08
+    m, h, plan = host_tables(cells, p, numbering="optimized", deform=amp, components=3)
+    rng = np.random.default_rng(5)
+    u = rng.uniform(-1, 1, h.n_dofs)
+    b = rng.uniform(-1, 1, h.n_dofs)
+    b[h.constrained_dofs] = 0.0
+    out = {}
+    variants = ("final_tensor_load", "inverse_jacobian_load")
+    for flag in ("0", "1"):
+        monkeypatch.setenv("MFCG_COMP_INTERLEAVE", flag)
+        for variant in variants:
+            op = gpu_operator(m, h, plan, p, nq, variant=variant)
+            res = S.solve("combined_pcg", op, b, minv=op.compute_diagonal(), config=S.SolverConfig(fixed_iterations=25))
+            std = S.solve("pcg", op, b, minv=op.compute_diagonal(), config=S.SolverConfig(fixed_iterations=25))
+            out[flag, variant] = (op.apply(u), hist_array(res.history), res.x, hist_array(std.history))
+    for variant in variants:
+        a0, h0, x0, s0 = out["0", variant]
+        a1, h1, x1, s1 = out["1", variant]
+        assert rel(a1, a0) < 1e-14 and rel(h1[:, 3], h0[:, 3]) < 1e-11 and rel(x1, x0) < 1e-11
+        assert rel(s1[:, 3], s0[:, 3]) < 1e-11
+        # components must not mix: component c of A u is the scalar operator on component c
+        assert rel(h1[:12, 3], s1[:12, 3]) < 1e-6
+
+
 def test_three_components_midsize_vs_oracle():
     """Q5, ragged brick grid, three components against the CPU oracle; a vector whose components
     differ must not mix them."""
