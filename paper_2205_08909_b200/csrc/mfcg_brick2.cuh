@@ -74,6 +74,9 @@ template <int ID, int COUNT> __device__ __forceinline__ void named_arrive() {
 #ifndef MFCG_B2_UNR
 #define MFCG_B2_UNR 2
 #endif
+#ifndef MFCG_B2_PMIN
+#define MFCG_B2_PMIN 4  // lowest degree that runs in the persistent kernel
+#endif
 #ifndef MFCG_B2_REGTAB
 #define MFCG_B2_REGTAB 1  // update warps keep their granules' table entries in registers (fp64, shared planes)
 #endif
@@ -101,7 +104,7 @@ template <int P> struct Brick2Enabled {
   // Measured at ~5e7 DoFs (profiles/r02_sweeps.txt): p = 5 +5 %, p = 4 +1 %, but p = 3 / 2 -13 / -10 % against
   // the first-generation kernel (many small planes per layer: the per-plane hand-over costs more than the
   // register-resident sweeps save), so the low degrees stay there.
-  static constexpr bool value = (P >= 4 && P <= 5) && (Cfg<P, 0>::BX * Cfg<P, 0>::BY) % 16 == 0;
+  static constexpr bool value = (P >= MFCG_B2_PMIN && P <= 5) && (Cfg<P, 0>::BX * Cfg<P, 0>::BY) % 16 == 0;
 };
 
 template <int P, typename T> struct Geo2 {
