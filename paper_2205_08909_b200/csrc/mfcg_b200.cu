@@ -198,10 +198,6 @@ static int op_create_impl(mfcg_ctx* ctx, const mfcg_op_desc* d, mfcg_op* op) {
     set_error("vector length does not match handler");
     return MFCG_EINVAL;
   }
-  if (C > 1 && (d->slab_z0 != 0 || (d->global_cells_z > 0 && d->global_cells_z != d->cells[2]))) {
-    set_error("z-slabs of a 3-component operator are not supported");
-    return MFCG_EUNSUPPORTED;
-  }
   c.ncomp = C;
   if (d->n_dofs / C >= (i64)2147483647) { set_error("more than 2^31-1 DoFs per GPU are not supported"); return MFCG_EUNSUPPORTED; }
   c.p = p;

@@ -505,7 +505,7 @@ class Engine : public EngineBase {
     const i64 nxy = (i64)(c_->grid.cells[0] * P + 1) * (c_->grid.cells[1] * P + 1);
     for (int side = 0; side < 2; ++side)
       for (int rv = 0; rv < 2; ++rv)
-        if (!plane_[side][rv]) MFCG_CUDA(cudaMalloc(&plane_[side][rv], sizeof(double) * nxy));
+        if (!plane_[side][rv]) MFCG_CUDA(cudaMalloc(&plane_[side][rv], sizeof(double) * nxy * C_));
     if (!d_sums_) MFCG_CUDA(cudaMalloc(&d_sums_, sizeof(double) * 8));
     if (!ev_front_) MFCG_CUDA(cudaEventCreateWithFlags(&ev_front_, cudaEventDisableTiming));
     return ensure_vectors(true);
@@ -514,7 +514,7 @@ class Engine : public EngineBase {
   void* g_plane(int side, int recv) override { return plane_[side][recv]; }
   size_t g_plane_bytes(bool diag_planes) override {
     const size_t nxy = (size_t)(c_->grid.cells[0] * P + 1) * (c_->grid.cells[1] * P + 1);
-    return nxy * (diag_planes ? sizeof(double) : sizeof(T));
+    return nxy * (diag_planes ? sizeof(double) : sizeof(T) * (size_t)C_);  // the diagonal is one value per node
   }
   double* g_sums() override { return d_sums_; }
 
@@ -538,8 +538,8 @@ class Engine : public EngineBase {
     const BrickGrid& g = c_->grid;
     const i64 nb = c_->n_bricks, nxy = (i64)g.mb[0] * g.mb[1];
     if (g.n_dofs > g.n_int) {
-      k_surface_init<T><<<vgrid_, VT, 0, stream()>>>(g, v_);
-      ++launches_;
+      for (int c = 0; c < C_; ++c) k_surface_init<T><<<vgrid_, VT, 0, stream()>>>(g, v_ + c * cs_);
+      launches_ += C_;
     }
     if (g.mb[2] <= 2) {
       if ((rc = launch_brick(0, p_, nullptr, v_, nullptr))) return rc;
@@ -556,8 +556,8 @@ class Engine : public EngineBase {
   int g_apply_end(double* dst, int location) override {
     const BrickGrid& g = c_->grid;
     if (g.n_dofs > g.n_int) {
-      k_surface_fix<T><<<vgrid_, VT, 0, stream()>>>(g, p_, v_);
-      ++launches_;
+      for (int c = 0; c < C_; ++c) k_surface_fix<T><<<vgrid_, VT, 0, stream()>>>(g, p_ + c * cs_, v_ + c * cs_);
+      launches_ += C_;
     }
     int rc = store_vec(v_, dst, location);
     if (rc) return rc;
@@ -569,15 +569,18 @@ class Engine : public EngineBase {
   int pack_planes(bool diag_planes) {
     cudaStream_t cs = c_->ctx->comm_stream;
     const int Ktop = c_->grid.cells[2] * P;
-    if (c_->has_lower) {
-      if (diag_planes) k_plane_pack<double><<<vgrid_, VT, 0, cs>>>(c_->grid, 0, diag_raw_, (double*)plane_[0][0]);
-      else k_plane_pack<T><<<vgrid_, VT, 0, cs>>>(c_->grid, 0, v_, (T*)plane_[0][0]);
-      ++launches_;
-    }
-    if (c_->has_upper) {
-      if (diag_planes) k_plane_pack<double><<<vgrid_, VT, 0, cs>>>(c_->grid, Ktop, diag_raw_, (double*)plane_[1][0]);
-      else k_plane_pack<T><<<vgrid_, VT, 0, cs>>>(c_->grid, Ktop, v_, (T*)plane_[1][0]);
-      ++launches_;
+    const i64 nxy = (i64)(c_->grid.cells[0] * P + 1) * (c_->grid.cells[1] * P + 1);
+    for (int side = 0; side < 2; ++side) {
+      if (!(side == 0 ? c_->has_lower : c_->has_upper)) continue;
+      const int K = side == 0 ? 0 : Ktop;
+      if (diag_planes) {
+        k_plane_pack<double><<<vgrid_, VT, 0, cs>>>(c_->grid, K, diag_raw_, (double*)plane_[side][0]);
+        ++launches_;
+      } else {
+        for (int c = 0; c < C_; ++c)  // component fields one after the other in the plane buffer
+          k_plane_pack<T><<<vgrid_, VT, 0, cs>>>(c_->grid, K, v_ + c * cs_, (T*)plane_[side][0] + c * nxy);
+        launches_ += C_;
+      }
     }
     MFCG_CUDA(cudaGetLastError());
     return MFCG_OK;
@@ -596,8 +599,11 @@ class Engine : public EngineBase {
     const BrickGrid& g = c_->grid;
     const i64 n = g.n_dofs, nb = c_->n_bricks, nxy = (i64)g.mb[0] * g.mb[1];
     if (n > g.n_int) {
-      k_pre<T><<<vgrid_, VT, 0, stream()>>>(g, g.n_int, n, 1, r_, p_, v_, x_, minv_, c_->d_state);
-      ++launches_;
+      for (int c = 0; c < C_; ++c) {
+        const i64 o = c * cs_;
+        k_pre<T><<<vgrid_, VT, 0, stream()>>>(g, g.n_int, n, 1, r_ + o, p_ + o, v_ + o, x_ + o, minv_ + o, c_->d_state);
+      }
+      launches_ += C_;
     }
     int rc;
     if (g.mb[2] <= 2) {
@@ -617,15 +623,18 @@ class Engine : public EngineBase {
   int g_unpack(bool diag_planes) override {
     cudaStream_t cs = c_->ctx->comm_stream;
     const int Ktop = c_->grid.cells[2] * P;
-    if (c_->has_lower) {
-      if (diag_planes) k_plane_add<double><<<vgrid_, VT, 0, cs>>>(c_->grid, 0, diag_raw_, (const double*)plane_[0][1]);
-      else k_plane_add<T><<<vgrid_, VT, 0, cs>>>(c_->grid, 0, v_, (const T*)plane_[0][1]);
-      ++launches_;
-    }
-    if (c_->has_upper) {
-      if (diag_planes) k_plane_add<double><<<vgrid_, VT, 0, cs>>>(c_->grid, Ktop, diag_raw_, (const double*)plane_[1][1]);
-      else k_plane_add<T><<<vgrid_, VT, 0, cs>>>(c_->grid, Ktop, v_, (const T*)plane_[1][1]);
-      ++launches_;
+    const i64 nxy = (i64)(c_->grid.cells[0] * P + 1) * (c_->grid.cells[1] * P + 1);
+    for (int side = 0; side < 2; ++side) {
+      if (!(side == 0 ? c_->has_lower : c_->has_upper)) continue;
+      const int K = side == 0 ? 0 : Ktop;
+      if (diag_planes) {
+        k_plane_add<double><<<vgrid_, VT, 0, cs>>>(c_->grid, K, diag_raw_, (const double*)plane_[side][1]);
+        ++launches_;
+      } else {
+        for (int c = 0; c < C_; ++c)
+          k_plane_add<T><<<vgrid_, VT, 0, cs>>>(c_->grid, K, v_ + c * cs_, (const T*)plane_[side][1] + c * nxy);
+        launches_ += C_;
+      }
     }
     MFCG_CUDA(cudaGetLastError());
     return MFCG_OK;
@@ -635,12 +644,15 @@ class Engine : public EngineBase {
   int g_post() override {
     const BrickGrid& g = c_->grid;
     const i64 n = g.n_dofs;
-    int rows = (int)c_->n_bricks;
+    // rows of partial sums: per component, one per brick and one per k_post block (unused rows stay zero)
+    const int rows = (int)(rows_pc_ * C_);
     if (n > g.n_int) {
-      k_post<T><<<vgrid_, VT, 0, stream()>>>(g, g.n_int, n, 1, r_, p_, v_, minv_, c_->d_state,
-                                             partials_a_ + 8 * c_->n_bricks);
-      rows += vgrid_;
-      ++launches_;
+      for (int c = 0; c < C_; ++c) {
+        const i64 o = c * cs_;
+        k_post<T><<<vgrid_, VT, 0, stream()>>>(g, g.n_int, n, 1, r_ + o, p_ + o, v_ + o, minv_ + o, c_->d_state,
+                                               partials_a_ + 8 * (c * rows_pc_ + c_->n_bricks));
+      }
+      launches_ += C_;
     }
     k_reduce_partials<<<1, 256, 0, stream()>>>(partials_a_, rows, 7, 0, d_sums_);
     ++launches_;
@@ -662,6 +674,16 @@ class Engine : public EngineBase {
     return MFCG_OK;
   }
 
+  // a.b over the DoFs this slab owns, all components -> out[0]
+  int dot_owned(const T* a, const T* b, double* partials, double* out) {
+    for (int c = 0; c < C_; ++c)
+      k_dot_owned<T><<<vgrid_, VT, 0, stream()>>>(c_->grid, a + c * cs_, b + c * cs_, partials + 8 * (i64)c * vgrid_);
+    k_reduce_partials<<<1, 256, 0, stream()>>>(partials, vgrid_ * C_, 1, 0, out);
+    launches_ += C_ + 1;
+    MFCG_CUDA(cudaGetLastError());
+    return MFCG_OK;
+  }
+
   // right-hand side, preconditioner, zero vectors, this slab's part of b.b
   int g_begin(const mfcg_solve_args* a, int limit) override {
     const i64 n = c_->grid.n_dofs;
@@ -680,23 +702,22 @@ class Engine : public EngineBase {
     tab_.diag_onfly = (prec && !a->inv_diag && !general_) ? 1 : 0;
     use_brick2_ = brick2_ok_ && (tab_.diag_onfly || !prec);
     if (prec) {
-      if (a->inv_diag) {
-        if ((rc = load_vec(a->inv_diag, a->location, minv_))) return rc;
+      if (a->inv_diag) {  // one value per node (solvers.py:617-621), replicated into the component fields
+        if ((rc = load_vec(a->inv_diag, a->location, minv_, 1))) return rc;
       } else {
-        k_convert<T, double><<<vgrid_, VT, 0, stream()>>>(n, c_->d_invdiag, minv_);
-        ++launches_;
+        for (int c = 0; c < C_; ++c) k_convert<T, double><<<vgrid_, VT, 0, stream()>>>(n, c_->d_invdiag, minv_ + c * cs_);
+        launches_ += C_;
       }
     } else {
-      k_fill<T><<<vgrid_, VT, 0, stream()>>>(n, minv_, (T)1);
+      k_fill<T><<<vgrid_, VT, 0, stream()>>>(nt_, minv_, (T)1);
       ++launches_;
     }
-    MFCG_CUDA(cudaMemsetAsync(x_, 0, sizeof(T) * n, stream()));
-    MFCG_CUDA(cudaMemsetAsync(p_, 0, sizeof(T) * n, stream()));
-    MFCG_CUDA(cudaMemsetAsync(v_, 0, sizeof(T) * n, stream()));
-    k_dot_owned<T><<<vgrid_, VT, 0, stream()>>>(c_->grid, r_, r_, partials_a_);
-    k_reduce_partials<<<1, 256, 0, stream()>>>(partials_a_, vgrid_, 1, 0, d_sums_);
-    launches_ += 2;
-    MFCG_CUDA(cudaGetLastError());
+    MFCG_CUDA(cudaMemsetAsync(x_, 0, sizeof(T) * nt_, stream()));
+    MFCG_CUDA(cudaMemsetAsync(p_, 0, sizeof(T) * nt_, stream()));
+    MFCG_CUDA(cudaMemsetAsync(v_, 0, sizeof(T) * nt_, stream()));
+    if ((rc = dot_owned(r_, r_, partials_a_, d_sums_))) return rc;
+    // rows no kernel of the iteration writes must read as zero in g_post
+    MFCG_CUDA(cudaMemsetAsync(partials_a_, 0, sizeof(double) * 8 * rows_pc_ * C_, stream()));
     return MFCG_OK;
   }
 
@@ -736,23 +757,23 @@ class Engine : public EngineBase {
     if ((rc = load_vec(a->b, a->location, v_))) return rc;   // b is staged in v, as in run_standard
     if (std_prec_) {
       if (a->inv_diag) {
-        if ((rc = load_vec(a->inv_diag, a->location, minv_))) return rc;
+        if ((rc = load_vec(a->inv_diag, a->location, minv_, 1))) return rc;
       } else {
-        k_convert<T, double><<<vgrid_, VT, 0, stream()>>>(n, c_->d_invdiag, minv_);
-        ++launches_;
+        for (int c = 0; c < C_; ++c) k_convert<T, double><<<vgrid_, VT, 0, stream()>>>(n, c_->d_invdiag, minv_ + c * cs_);
+        launches_ += C_;
       }
     }
-    k_dot_owned<T><<<vgrid_, VT, 0, stream()>>>(c_->grid, v_, v_, partials_a_);
-    k_reduce_partials<<<1, 256, 0, stream()>>>(partials_a_, vgrid_, 1, 0, d_sums_);   // b.b of this slab
-    launches_ += 2;
-    MFCG_CUDA(cudaGetLastError());
-    return MFCG_OK;
+    return dot_owned(v_, v_, partials_a_, d_sums_);   // b.b of this slab
   }
   // after g_set_state: r = b, z = M r, p = z, x = 0 and this slab's r.z, r.r
   int g_std_init_vectors() override {
-    k_std_init_owned<T><<<vgrid_, VT, 0, stream()>>>(c_->grid, v_, std_prec_ ? minv_ : nullptr, r_, z_, p_, x_, partials_a_);
-    k_reduce_partials<<<1, 256, 0, stream()>>>(partials_a_, vgrid_, 2, 0, d_sums_);
-    launches_ += 2;
+    for (int c = 0; c < C_; ++c) {
+      const i64 o = c * cs_;
+      k_std_init_owned<T><<<vgrid_, VT, 0, stream()>>>(c_->grid, v_ + o, std_prec_ ? minv_ + o : nullptr, r_ + o, z_ + o,
+                                                       p_ + o, x_ + o, partials_a_ + 8 * (i64)c * vgrid_);
+    }
+    k_reduce_partials<<<1, 256, 0, stream()>>>(partials_a_, vgrid_ * C_, 2, 0, d_sums_);
+    launches_ += C_ + 1;
     MFCG_CUDA(cudaGetLastError());
     return MFCG_OK;
   }
@@ -767,8 +788,8 @@ class Engine : public EngineBase {
     const i64 nb = c_->n_bricks, nxy = (i64)g.mb[0] * g.mb[1];
     int rc;
     if (g.n_dofs > g.n_int) {
-      k_surface_init<T><<<vgrid_, VT, 0, stream()>>>(g, v_);
-      ++launches_;
+      for (int c = 0; c < C_; ++c) k_surface_init<T><<<vgrid_, VT, 0, stream()>>>(g, v_ + c * cs_);
+      launches_ += C_;
     }
     if (g.mb[2] <= 2) {
       if ((rc = launch_brick(0, p_, nullptr, v_, nullptr))) return rc;
@@ -785,21 +806,15 @@ class Engine : public EngineBase {
   int g_std_apply_end() override {
     const BrickGrid& g = c_->grid;
     if (g.n_dofs > g.n_int) {
-      k_surface_fix<T><<<vgrid_, VT, 0, stream()>>>(g, p_, v_);
-      ++launches_;
+      for (int c = 0; c < C_; ++c) k_surface_fix<T><<<vgrid_, VT, 0, stream()>>>(g, p_ + c * cs_, v_ + c * cs_);
+      launches_ += C_;
     }
     MFCG_CUDA(cudaGetLastError());
     return MFCG_OK;
   }
-  int g_std_dot_pv() override {
-    k_dot_owned<T><<<vgrid_, VT, 0, stream()>>>(c_->grid, p_, v_, partials_a_);
-    k_reduce_partials<<<1, 256, 0, stream()>>>(partials_a_, vgrid_, 1, 0, d_sums_);
-    launches_ += 2;
-    MFCG_CUDA(cudaGetLastError());
-    return MFCG_OK;
-  }
+  int g_std_dot_pv() override { return dot_owned(p_, v_, partials_a_, d_sums_); }
   int g_std_alpha_update(const double* global_sums_dev) override {
-    const i64 n = c_->grid.n_dofs;
+    const i64 n = nt_;  // flat over the component fields
     k_std_alpha<<<1, 256, 0, stream()>>>(global_sums_dev, 1, c_->d_state);
     k_std_axpy<T><<<vgrid_, VT, 0, stream()>>>(n, x_, p_, 1.0, c_->d_state);
     k_std_axpy<T><<<vgrid_, VT, 0, stream()>>>(n, r_, v_, -1.0, c_->d_state);
@@ -809,22 +824,20 @@ class Engine : public EngineBase {
   }
   // this slab's r.r (sum 0) and r.z (sum 1; = r.r without preconditioner)
   int g_std_dots_r() override {
-    const i64 n = c_->grid.n_dofs;
-    k_dot_owned<T><<<vgrid_, VT, 0, stream()>>>(c_->grid, r_, r_, partials_a_);
-    k_reduce_partials<<<1, 256, 0, stream()>>>(partials_a_, vgrid_, 1, 0, d_sums_);
-    launches_ += 2;
+    const i64 n = nt_;
+    int rc = dot_owned(r_, r_, partials_a_, d_sums_);
+    if (rc) return rc;
     if (std_prec_) {
       k_std_prec<T><<<vgrid_, VT, 0, stream()>>>(n, z_, minv_, r_, c_->d_state);
-      k_dot_owned<T><<<vgrid_, VT, 0, stream()>>>(c_->grid, r_, z_, partials_b_);
-      k_reduce_partials<<<1, 256, 0, stream()>>>(partials_b_, vgrid_, 1, 0, d_sums_ + 1);
-      launches_ += 3;
+      ++launches_;
+      if ((rc = dot_owned(r_, z_, partials_b_, d_sums_ + 1))) return rc;
     }
     MFCG_CUDA(cudaGetLastError());
     return MFCG_OK;
   }
   // global_sums_dev: row 0 = (r.r, r.z)
   int g_std_beta_p(const double* global_sums_dev) override {
-    const i64 n = c_->grid.n_dofs;
+    const i64 n = nt_;
     k_std_beta_sums<<<1, 32, 0, stream()>>>(global_sums_dev, std_prec_ ? 1 : 0, c_->d_state, d_history_);
     k_std_update_p<T><<<vgrid_, VT, 0, stream()>>>(n, p_, std_prec_ ? z_ : r_, c_->d_state);
     launches_ += 2;

@@ -108,8 +108,6 @@ class MatrixFreeOperator:
             raise NotImplementedError(
                 "the B200 hot path covers the Laplace operator (SURVEY.md section 8); "
                 "mass equations are out of scope")
-        if spec.components == 3 and (slab_z0 or (global_cells_z and global_cells_z != mesh.cells_per_dim[2])):
-            raise NotImplementedError("z-slabs of a 3-component operator are not supported")
         if precision not in ("fp64", "fp32"):
             raise ValueError("precision must be 'fp64' or 'fp32'")
         self.spec = spec

@@ -71,22 +71,27 @@ def _lattice_ids(handler: DofHandler, z0: int):
     return idx.ravel(), I, J, K
 
 
-def build_slab(global_mesh: HexMesh, p: int, z0: int, nz_g: int, constrain_boundary: bool = True) -> Slab:
+def build_slab(global_mesh: HexMesh, p: int, z0: int, nz_g: int, constrain_boundary: bool = True,
+               components: int = 1) -> Slab:
     """Tables of one slab: the slab mesh, its handler with the global Dirichlet set restricted to
-    the slab (interface planes are NOT constrained), and the local->global lattice map."""
+    the slab (interface planes are NOT constrained), and the local->global lattice map (per node;
+    with 3 components unknown ``3 * node + c`` of the slab is unknown ``3 * global_node + c`` of the mesh)."""
     nx, ny, nz = global_mesh.cells_per_dim
     mesh = replace(build_cartesian_mesh((nx, ny, nz_g), global_mesh.extents),
                    extents=global_mesh.extents, deformation=global_mesh.deformation)
-    h = dofs.distribute_dofs(mesh, p, 1, constrain_boundary=False)
-    node, I, J, K = _lattice_ids(h, z0)
+    hs = dofs.distribute_dofs(mesh, p, 1, constrain_boundary=False)
+    node, I, J, K = _lattice_ids(hs, z0)
     NX, NY, NZ = nx * p + 1, ny * p + 1, nz * p + 1
-    glob = np.empty(h.n_dofs, dtype=np.int64)
+    glob = np.empty(hs.n_dofs, dtype=np.int64)
     glob[node] = I + NX * (J + NY * K)
     constrained = np.empty(0, dtype=np.int64)
     if constrain_boundary:
         on = (I == 0) | (I == NX - 1) | (J == 0) | (J == NY - 1) | (K == 0) | (K == NZ - 1)
         constrained = np.unique(node[on])
-    h = DofHandler(h.n_dofs, 1, p, mesh.cells_per_dim, h.cell_index_blocks, constrained)
+    h = hs if components == 1 else dofs.distribute_dofs(mesh, p, components, constrain_boundary=False)
+    if components > 1:  # constraints cover whole nodes (dofs.py:174-178)
+        constrained = (constrained[:, None] * components + np.arange(components)[None, :]).ravel()
+    h = DofHandler(h.n_dofs, components, p, mesh.cells_per_dim, h.cell_index_blocks, constrained)
     return Slab(mesh, h, z0, nz, glob)
 
 
@@ -140,14 +145,15 @@ class SlabGroup:
         return dsts
 
     def compute_diagonal(self):
-        outs = [np.empty(op.n_dofs) for op in self.ops]
+        outs = [np.empty(op.n_dofs // op.components) for op in self.ops]   # one value per node (operator.py:90)
         _lib.check(self._lib.mfcg_diagonal_group(self._handles, len(self.ops), self._ptr_array(outs), 0))
         return outs
 
     def solve(self, variant, bs, config=None, *, location=0, xs=None, minvs=None, outs=None):
         """(P)CG on the whole mesh, merged (`combined_cg`, `combined_pcg`) or standard (`cg`, `pcg`); returns one
         SolveResult per slab (same history).  ``minvs``: one caller-supplied inverse diagonal per slab (host arrays,
-        one value per node) instead of the operator's own Jacobi diagonal."""
+        one value per node) instead of the operator's own Jacobi diagonal.  Operators with 3 components (BP4 type)
+        take interleaved vectors, as everywhere in the package."""
         from .solvers import SolveResult, SolverBreakdown, SolverConfig, _BREAKDOWN_TEXT
         cfg = config or SolverConfig()
         n = len(self.ops)
@@ -175,7 +181,7 @@ class SlabGroup:
                 if location != 0:
                     raise ValueError("caller-supplied preconditioners are host arrays (location=0)")
                 md = np.ascontiguousarray(getattr(minvs[g], "inverse_diagonal", minvs[g]), dtype=np.float64)
-                if len(md) != op.n_dofs:
+                if len(md) != op.n_dofs // op.components:   # one value per node (solvers.py:617-621)
                     raise ValueError("preconditioner length does not match operator")
                 keep.append(md)
                 a.inv_diag = md.ctypes.data

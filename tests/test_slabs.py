@@ -198,6 +198,68 @@ def test_slab_group_equals_single_slab_on_one_gpu(cells, p, G, deform):
     assert all(abs(r.iterations - one.iterations) <= 1 and r.converged for r in many)
 
 
+def test_three_component_slab_tables():
+    """build_slab with 3 components: interleaved unknowns, whole-node constraints, per-node lattice map."""
+    m = pmesh.build_cartesian_mesh((3, 2, 6))
+    s1 = slabs.build_slab(m, 2, 2, 2)
+    s3 = slabs.build_slab(m, 2, 2, 2, components=3)
+    assert s3.handler.components == 3 and s3.handler.n_dofs == 3 * s1.handler.n_dofs
+    assert np.array_equal(s3.global_nodes, s1.global_nodes)
+    c1 = s1.handler.constrained_dofs
+    assert np.array_equal(s3.handler.constrained_dofs, (3 * c1[:, None] + np.arange(3)).ravel())
+    ref = dofs.distribute_dofs(s1.mesh, 2, 3, constrain_boundary=False)
+    assert np.array_equal(s3.handler.cell_index_blocks, ref.cell_index_blocks)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cells,p,G,deform", [((5, 4, 9), 5, 2, 0.0), ((4, 3, 8), 3, 3, 0.1)])
+def test_three_component_slab_group_equals_single_slab(cells, p, G, deform):
+    """BP4-type operator (3 components) on G slabs in lockstep against the one-slab operator: apply, merged PCG
+    and standard PCG; the interface planes of all three component fields travel in one buffer."""
+    from paper_2205_08909_b200 import solvers as S
+    from paper_2205_08909_b200.operator import MatrixFreeOperator, OperatorSpec
+    variant = "final_tensor_load" if deform else "affine"
+    m, h, plan = host_tables(cells, p, deform=deform, components=3)
+    op1 = gpu_operator(m, h, plan, p, p + 1, variant=variant)
+    hs = dofs.distribute_dofs(m, p, 1, constrain_boundary=True)
+    lat = _global_lattice_of(hs, p)
+    glob_of_lat = np.empty_like(lat)
+    glob_of_lat[lat] = np.arange(hs.n_dofs)
+    sl = [slabs.build_slab(m, p, z0, n, components=3) for z0, n in slabs.slab_layers(cells[2], G)]
+    ops = []
+    for s in sl:
+        plan_s = dofs.make_batches(s.mesh, dofs.batch_size(p, 3, 8), "morton")
+        ops.append(MatrixFreeOperator(OperatorSpec("laplace", 3, p, p + 1, pmesh.GeometryVariant(variant)),
+                                      s.mesh, s.handler, plan_s, slab_z0=s.z0, global_cells_z=s.global_cells_z))
+    node_maps = [glob_of_lat[s.global_nodes] for s in sl]
+    maps = [(3 * nm[:, None] + np.arange(3)[None, :]).ravel() for nm in node_maps]
+    group = slabs.SlabGroup(ops)
+    rng = np.random.default_rng(4)
+    u = rng.standard_normal(h.n_dofs)
+    ref = op1.apply(u)
+    for gl, out in zip(maps, group.apply([u[gl] for gl in maps])):
+        assert rel(out, ref[gl]) < 1e-12
+    dref = op1.compute_diagonal().inverse_diagonal          # one value per node
+    for nm, d in zip(node_maps, group.compute_diagonal()):
+        assert d.shape == nm.shape and rel(d, dref[nm]) < 1e-12
+    b = rng.uniform(-1, 1, h.n_dofs)
+    b[h.constrained_dofs] = 0.0
+    cfg = S.SolverConfig(fixed_iterations=30)
+    for name in ("combined_pcg", "pcg", "combined_cg"):
+        mv = op1.compute_diagonal() if name != "combined_cg" else None
+        one = S.solve(name, op1, b, minv=mv, config=cfg)
+        many = group.solve(name, [b[gl] for gl in maps], cfg)
+        H1 = hist_array(one.history)
+        for gl, r in zip(maps, many):
+            assert r.iterations == 30
+            assert rel(hist_array(r.history)[:25], H1[:25]) < 1e-10, name
+            assert rel(r.x, one.x[gl]) < 1e-9, name
+    custom = group.solve("combined_pcg", [b[gl] for gl in maps], cfg, minvs=[dref[nm] for nm in node_maps])
+    one = S.solve("combined_pcg", op1, b, minv=op1.compute_diagonal(), config=cfg)
+    for gl, r in zip(maps, custom):
+        assert rel(hist_array(r.history)[:25], hist_array(one.history)[:25]) < 1e-10
+
+
 @pytest.mark.gpu
 def test_nccl_binding_single_rank():
     """The run-time NCCL binding (dlopen of the libnccl torch ships): unique id, communicator with
