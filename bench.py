@@ -271,19 +271,20 @@ def run_slabs(args, rank, local_rank, world):
     cells = workload_cells(args, world)
     gmesh = pmesh.build_cartesian_mesh(cells)
     z0, nzg = slabs.slab_layers(cells[2], world)[rank]
-    slab = slabs.build_slab(gmesh, p, z0, nzg)
-    plan = dofs.make_batches(slab.mesh, dofs.batch_size(p, 1, 8), "morton")
+    nc = args.components
+    slab = slabs.build_slab(gmesh, p, z0, nzg, components=nc)
+    plan = dofs.make_batches(slab.mesh, dofs.batch_size(p, nc, 8), "morton")
     uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
     if rank == 0:
         uid.copy_(torch.frombuffer(bytearray(slabs.new_unique_id()), dtype=torch.uint8))
     dist.broadcast(uid, 0)
     slabs.init_comm(local_rank, bytes(uid.cpu().numpy().tobytes()), rank, world)
-    op = MatrixFreeOperator(OperatorSpec("laplace", 1, p, p + 1, pmesh.GeometryVariant.AFFINE), slab.mesh,
+    op = MatrixFreeOperator(OperatorSpec("laplace", nc, p, p + 1, pmesh.GeometryVariant.AFFINE), slab.mesh,
                             slab.handler, plan, device=local_rank, precision=args.precision,
                             brick=tuple(args.brick), slab_z0=z0, global_cells_z=cells[2])
     group = slabs.SlabGroup([op])
     n_local = slab.handler.n_dofs
-    n_global = int(np.prod([c * p + 1 for c in cells]))
+    n_global = int(np.prod([c * p + 1 for c in cells])) * nc
     # seeded RHS of the global problem in lattice order, restricted to the slab
     rng = np.random.default_rng(0)
     NX, NY = cells[0] * p + 1, cells[1] * p + 1
@@ -291,6 +292,8 @@ def run_slabs(args, rank, local_rank, world):
     rng.uniform(-1.0, 1.0, z0 * p * plane)                      # skip the lower slabs' part of the stream
     vals = rng.uniform(-1.0, 1.0, (nzg * p + 1) * plane)
     b = vals[slab.global_nodes - z0 * p * plane]
+    if nc > 1:  # interleaved components: the node's value scaled per component
+        b = (b[:, None] * (1.0 - 0.5 * np.arange(nc))[None, :]).ravel()
     b[slab.handler.constrained_dofs] = 0.0
     b_host = torch.from_numpy(b).pin_memory()
     b_dev = b_host.cuda()
@@ -357,7 +360,7 @@ def run_slabs(args, rank, local_rank, world):
                              "buffers, max over ranks"},
             "gpu_launches": int(launches), "clocks": clocks,
             "extra": {"final_relative_residual": res.residual, "dofs_per_gpu": n_local,
-                      "plane_bytes_per_exchange": 8 * plane, "bricks_per_gpu": info["n_bricks"],
+                      "plane_bytes_per_exchange": 8 * plane * nc, "bricks_per_gpu": info["n_bricks"],
                       "timer": "CUDA events on each rank's library stream, max over ranks"},
         }
         print(json.dumps(line))

@@ -279,7 +279,8 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
   unsigned long long tacc[6] = {0, 0, 0, 0, 0, 0}, tacc6 = 0;
 #endif
   for (int bi = blockIdx.x; bi < brick_count; bi += gridDim.x) {
-    const int b = brick_first + bi;
+    int b = brick_first + bi;  // a range may wrap around the end of the brick list (top then bottom brick layer of a slab)
+    if (b >= g.mb[0] * g.mb[1] * g.mb[2]) b -= g.mb[0] * g.mb[1] * g.mb[2];
     const int mx = b % g.mb[0];
     const int my = (b / g.mb[0]) % g.mb[1];
     const int mz = b / (g.mb[0] * g.mb[1]);

@@ -541,15 +541,7 @@ class Engine : public EngineBase {
       for (int c = 0; c < C_; ++c) k_surface_init<T><<<vgrid_, VT, 0, stream()>>>(g, v_ + c * cs_);
       launches_ += C_;
     }
-    if (g.mb[2] <= 2) {
-      if ((rc = launch_brick(0, p_, nullptr, v_, nullptr))) return rc;
-      MFCG_CUDA(cudaEventRecord(ev_front_, stream()));
-    } else {
-      if ((rc = launch_brick(0, p_, nullptr, v_, nullptr, 0, nxy))) return rc;
-      if ((rc = launch_brick(0, p_, nullptr, v_, nullptr, nb - nxy, nxy))) return rc;
-      MFCG_CUDA(cudaEventRecord(ev_front_, stream()));
-      if ((rc = launch_brick(0, p_, nullptr, v_, nullptr, nxy, nb - 2 * nxy))) return rc;
-    }
+    if ((rc = launch_interface_first(0, p_, nullptr, v_, nullptr))) return rc;
     MFCG_CUDA(cudaStreamWaitEvent(c_->ctx->comm_stream, ev_front_, 0));
     return pack_planes(false);
   }
@@ -563,6 +555,26 @@ class Engine : public EngineBase {
     if (rc) return rc;
     MFCG_CUDA(cudaStreamSynchronize(stream()));
     return MFCG_OK;
+  }
+
+  // Brick launches of a slab: the brick layers that touch an interface plane first (one launch: the top layer, then,
+  // wrapping around the end of the brick list, the bottom layer), the event that releases the communication
+  // stream, then the rest.  A slab without neighbours, or of at most two brick layers, goes out as one launch.
+  int launch_interface_first(int mode, const T* src, T* pv, T* v, double* partials) {
+    const BrickGrid& g = c_->grid;
+    const i64 nb = c_->n_bricks, nxy = (i64)g.mb[0] * g.mb[1];
+    const bool lo = c_->has_lower, hi = c_->has_upper;
+    int rc;
+    if (g.mb[2] <= 2 || (!lo && !hi)) {
+      if ((rc = launch_brick(mode, src, pv, v, partials))) return rc;
+      MFCG_CUDA(cudaEventRecord(ev_front_, stream()));
+      return MFCG_OK;
+    }
+    const i64 first = hi ? nb - nxy : 0, count = (lo && hi) ? 2 * nxy : nxy;
+    if ((rc = launch_brick(mode, src, pv, v, partials, first, count))) return rc;
+    MFCG_CUDA(cudaEventRecord(ev_front_, stream()));
+    const i64 rest_first = lo ? nxy : 0;   // interior layers (+ the far layer of a slab with one neighbour)
+    return launch_brick(mode, src, pv, v, partials, rest_first, nb - count);
   }
 
   // pack the interface planes of v (or of the raw diagonal) on the communication stream
@@ -606,15 +618,7 @@ class Engine : public EngineBase {
       launches_ += C_;
     }
     int rc;
-    if (g.mb[2] <= 2) {
-      if ((rc = launch_brick(1, nullptr, p_, v_, partials_a_))) return rc;
-      MFCG_CUDA(cudaEventRecord(ev_front_, stream()));
-    } else {
-      if ((rc = launch_brick(1, nullptr, p_, v_, partials_a_, 0, nxy))) return rc;
-      if ((rc = launch_brick(1, nullptr, p_, v_, partials_a_, nb - nxy, nxy))) return rc;
-      MFCG_CUDA(cudaEventRecord(ev_front_, stream()));
-      if ((rc = launch_brick(1, nullptr, p_, v_, partials_a_, nxy, nb - 2 * nxy))) return rc;
-    }
+    if ((rc = launch_interface_first(1, nullptr, p_, v_, partials_a_))) return rc;
     MFCG_CUDA(cudaStreamWaitEvent(cs, ev_front_, 0));
     return pack_planes(false);
   }
@@ -791,15 +795,7 @@ class Engine : public EngineBase {
       for (int c = 0; c < C_; ++c) k_surface_init<T><<<vgrid_, VT, 0, stream()>>>(g, v_ + c * cs_);
       launches_ += C_;
     }
-    if (g.mb[2] <= 2) {
-      if ((rc = launch_brick(0, p_, nullptr, v_, nullptr))) return rc;
-      MFCG_CUDA(cudaEventRecord(ev_front_, stream()));
-    } else {
-      if ((rc = launch_brick(0, p_, nullptr, v_, nullptr, 0, nxy))) return rc;
-      if ((rc = launch_brick(0, p_, nullptr, v_, nullptr, nb - nxy, nxy))) return rc;
-      MFCG_CUDA(cudaEventRecord(ev_front_, stream()));
-      if ((rc = launch_brick(0, p_, nullptr, v_, nullptr, nxy, nb - 2 * nxy))) return rc;
-    }
+    if ((rc = launch_interface_first(0, p_, nullptr, v_, nullptr))) return rc;
     MFCG_CUDA(cudaStreamWaitEvent(c_->ctx->comm_stream, ev_front_, 0));
     return pack_planes(false);
   }

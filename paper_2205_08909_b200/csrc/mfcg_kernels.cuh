@@ -607,7 +607,8 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
     if (Minv) Minv += o;
     if (partials) partials += comp * part_stride;
   }
-  const int b = bidx + brick_offset;  // slab runs launch the interface brick layers first
+  int b = bidx + brick_offset;  // slab runs launch the interface brick layers first; a range may wrap around
+  if (b >= g.mb[0] * g.mb[1] * g.mb[2]) b -= g.mb[0] * g.mb[1] * g.mb[2];
   const int mx = b % g.mb[0];
   const int my = (b / g.mb[0]) % g.mb[1];
   const int mz = b / (g.mb[0] * g.mb[1]);
