@@ -1212,7 +1212,7 @@ int Engine<P, T>::solve(const mfcg_solve_args* a, mfcg_solve_result* res) {
     cudaMemcpyFromSymbol(h, g_phase_cycles, sizeof(h));
 #if 1
     const char* names[24] = {"S.wait_lfull", "S.compute", "S.wait_tiles", "S.store", "M.wait_tiles", "M.zsweep", "M.gather", "M.barrier",
-                             "P.wait_tupd", "P.wait_ldone", "P.issue", "", "U.wait_ldone", "U.wait_tfull", "U.update", "U.perim_issue", "U.tail", "U.reduce+arrive", "S.bnd_issue", "S.bnd_wait", "S.bnd_barrier", "", "", ""};
+                             "P.wait_tupd", "P.wait_ldone", "P.issue", "", "U.wait_ldone", "U.wait_tfull", "U.update", "", "U.tail", "U.reduce+arrive", "S.bnd_issue", "S.bnd_wait", "S.bnd_barrier", "", "", ""};
 #else
     const char* names[16] = {"P.wait_empty", "P.fill", "P.post", "", "C.wait_full", "C.x", "C.y", "C.z", "C.bar", "C.gather",
                              "", "", "", "", "", ""};

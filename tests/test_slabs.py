@@ -139,9 +139,12 @@ def test_slab_renumbering_with_remote_category(cells, p, G):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("cells,p,G,deform", [((5, 4, 9), 5, 2, 0.0), ((6, 5, 12), 3, 3, 0.0),
-                                              ((4, 4, 17), 5, 4, 0.0), ((4, 3, 6), 3, 2, 0.1)])
-def test_slab_group_equals_single_slab_on_one_gpu(cells, p, G, deform):
+@pytest.mark.parametrize("cells,p,G,deform,bz", [((5, 4, 9), 5, 2, 0.0, 0), ((6, 5, 12), 3, 3, 0.0, 0),
+                                                 ((4, 4, 17), 5, 4, 0.0, 0), ((4, 3, 6), 3, 2, 0.1, 0),
+                                                 # bricks one cell layer deep: slabs of 4-5 brick layers, so the
+                                                 # interface layers go out first (middle slabs: one wrap-around launch)
+                                                 ((5, 4, 13), 5, 3, 0.0, 1), ((4, 3, 9), 3, 2, 0.1, 1)])
+def test_slab_group_equals_single_slab_on_one_gpu(cells, p, G, deform, bz):
     """G slabs stepped in lockstep on one GPU (device-to-device plane copies stand in for NCCL)
     against the one-slab operator: apply and diagonal at 1e-12, merged-CG history at 1e-10."""
     from paper_2205_08909_b200 import solvers as S
@@ -160,7 +163,9 @@ def test_slab_group_equals_single_slab_on_one_gpu(cells, p, G, deform):
         plan_s = dofs.make_batches(s.mesh, dofs.batch_size(p, 1, 8), "morton")
         ops.append(MatrixFreeOperator(OperatorSpec("laplace", 1, p, p + 1, pmesh.GeometryVariant(variant)),
                                       s.mesh, s.handler, plan_s, slab_z0=s.z0,
-                                      global_cells_z=s.global_cells_z))
+                                      global_cells_z=s.global_cells_z, brick=(0, 0, bz)))
+    if bz:
+        assert all(o.info()["brick"][2] == bz and o.info()["n_bricks"] >= 3 for o in ops)
     maps = [glob_of_lat[s.global_nodes] for s in sl]
     group = slabs.SlabGroup(ops)
     u = np.random.default_rng(3).standard_normal(h.n_dofs)
