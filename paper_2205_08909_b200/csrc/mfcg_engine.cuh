@@ -209,6 +209,8 @@ class Engine : public EngineBase {
       smem_ = (int)Geo<P, 1>::template smem_bytes<T>();
       MFCG_CUDA(cudaFuncSetAttribute(k_brick<P, T, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
       MFCG_CUDA(cudaFuncSetAttribute(k_brick<P, T, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
+      MFCG_CUDA(cudaFuncSetAttribute(k_brick<P, T, 0, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
+      MFCG_CUDA(cudaFuncSetAttribute(k_brick<P, T, 1, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
       MFCG_CUDA(cudaFuncSetAttribute(k_brick<P, T, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
       MFCG_CUDA(cudaFuncSetAttribute(k_brick<P, T, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
       int rc = build_general_tables();
@@ -424,10 +426,10 @@ class Engine : public EngineBase {
     if (C_ > 1 && general_ && !cellpath_ && c_->geometry != MFCG_GEOM_QUADRATIC_COMPUTE && comp_interleave_) {
       const i64 ps = 8 * rows_pc_;
       if (mode == 0)
-        k_brick<P, T, 0, 1><<<nb * C_, Cfg<P, 1>::THREADS, smem_, stream()>>>(
+        k_brick<P, T, 0, 1, true><<<nb * C_, Cfg<P, 1>::THREADS, smem_, stream()>>>(
             c_->grid, tab_, gen_, geo_, src, nullptr, v, nullptr, nullptr, nullptr, nullptr, nullptr, off, C_, cs_, ps);
       else
-        k_brick<P, T, 1, 1><<<nb * C_, Cfg<P, 1>::THREADS, smem_, stream()>>>(
+        k_brick<P, T, 1, 1, true><<<nb * C_, Cfg<P, 1>::THREADS, smem_, stream()>>>(
             c_->grid, tab_, gen_, geo_, nullptr, pv, v, r_, x_, minv_, c_->d_state, partials, off, C_, cs_, ps);
     } else
     for (int comp = 0; comp < C_; ++comp) {

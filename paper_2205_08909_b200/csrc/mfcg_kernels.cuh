@@ -549,7 +549,7 @@ template <int COUNT> __device__ __forceinline__ void math_barrier() {
 //                 memory, a deterministic gather of the cells' contributions per
 //                 lattice point, v stored (interior) or atomically added (shared).
 // Hand-over through two mbarrier pairs (full/empty per layer parity).
-template <int P, typename T, int MODE, int G>
+template <int P, typename T, int MODE, int G, bool MC = false>
 __global__ void __launch_bounds__(Cfg<P, G>::THREADS, Cfg<P, G>::MINB)
 k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAccess geo,
         const T* __restrict__ src, T* __restrict__ Pv,
@@ -594,8 +594,9 @@ k_brick(BrickGrid g, SepTables<T, P + 1> tab, GenTables<T, P + 1> gen, GeomAcces
 
   // ncomp > 1 (stored geometry, several components in one launch): consecutive blocks work on the same brick, one
   // component each, so the brick's geometry block comes from HBM once and from L2 for the other components
+  // (a separate instantiation, MC: adjusting the pointer arguments costs the single-component kernels registers)
   int bidx = blockIdx.x;
-  if (ncomp > 1) {
+  if constexpr (MC) {
     const int comp = bidx % ncomp;
     bidx /= ncomp;
     const i64 o = comp * comp_stride;
