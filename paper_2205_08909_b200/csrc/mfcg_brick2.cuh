@@ -53,6 +53,12 @@ __device__ __forceinline__ void pin_value(double& v) { asm volatile("" : "+d"(v)
 __device__ __forceinline__ void pin_value(float& v) { asm volatile("" : "+f"(v)); }
 __device__ __forceinline__ void pin_value(unsigned& v) { asm volatile("" : "+r"(v)); }
 template <class U> __device__ __forceinline__ void pin_value(U*& v) { asm volatile("" : "+l"(v)); }
+// one lane of a converged warp (elect.sync)
+__device__ __forceinline__ bool elect_one() {
+  unsigned pred = 0;
+  asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(pred));
+  return pred != 0;
+}
 template <int ID, int COUNT> __device__ __forceinline__ void named_barrier() {
   asm volatile("barrier.sync %0, %1;" ::"n"(ID), "n"(COUNT) : "memory");  // non-aligned: lanes of a warp may arrive from different places
 }
@@ -76,6 +82,9 @@ template <int ID, int COUNT> __device__ __forceinline__ void named_arrive() {
 #endif
 #ifndef MFCG_B2_PMIN
 #define MFCG_B2_PMIN 4  // lowest degree that runs in the persistent kernel
+#endif
+#ifndef MFCG_B2_UNIFORM_PRODUCER
+#define MFCG_B2_UNIFORM_PRODUCER 1  // producer warp runs converged, an elected lane issues the bulk copies
 #endif
 #ifndef MFCG_B2_REGTAB
 #define MFCG_B2_REGTAB 1  // update warps keep their granules' table entries in registers (fp64, shared planes)
@@ -305,6 +314,43 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
 
     if constexpr (ROLE == 1) {
       // ================================ producer ================================
+#if MFCG_B2_UNIFORM_PRODUCER
+      // The whole warp walks the planes with warp-uniform values; one elected lane issues.  (With a single active
+      // lane the compiler wraps every bulk copy into an election loop with five register-to-uniform moves.)
+      if (nplanes > 0) {
+        const i64 st_int = __shfl_sync(0xffffffffu, entity(13), 0);
+        for (int K = 1; K <= nplanes; ++K) {
+          const int q = q_base + K - 1, slot = q % NT;
+          B2_TIC(tp);
+          const int gf = g_base + K / P;  // layer whose gather finishes the plane
+          const i64 e0 = st_int + (i64)(K - 1) * nint2d;
+          const i64 a0 = e0 & ~(i64)(PER16 - 1);
+          const int off = (int)(e0 - a0);
+          const int len = (off + nint2d + PER16 - 1) & ~(PER16 - 1);
+          const unsigned bytes = (unsigned)(len * sizeof(T));
+          MFCG_CHECK(len <= PLB && a0 >= 0 && a0 + len <= g.n_dofs + 32 / (int)sizeof(T));
+          T* Rb = Rbuf + ((gf % NRL) * P + K % P) * PLB;
+          T* Pb = Tbuf + (slot * 3 + 0) * PLB;
+          T* Vb = Tbuf + (slot * 3 + 1) * PLB;
+          T* Xb = Tbuf + (slot * 3 + 2) * PLB;
+          const unsigned tx = bytes * (xmode ? 4u : 3u);
+          B2_TOC(tp, 2);
+          if (q >= NT) mbar_wait(&H.tupd[slot], ((q - NT) / NT) & 1);  // the slot's previous plane has been read
+          B2_TOC(tp, 0);
+          if ((K % P == 0 || K == 1) && gf >= NRL) mbar_wait(&H.ldone[(gf - NRL) & 3], ((gf - NRL) >> 2) & 1);
+          B2_TOC(tp, 1);
+          if (elect_one()) {
+            mbar_expect_tx(&H.tfull[slot], tx);
+            bulk_g2s(Rb, R + a0, bytes, &H.tfull[slot]);
+            bulk_g2s(Pb, Pv + a0, bytes, &H.tfull[slot]);
+            bulk_g2s(Vb, V + a0, bytes, &H.tfull[slot]);
+            if (xmode) bulk_g2s(Xb, X + a0, bytes, &H.tfull[slot]);
+          }
+          __syncwarp();
+          B2_TOC(tp, 2);
+        }
+      }
+#else
       if ((tid & 31) == 0 && nplanes > 0) {
         const i64 st_int = entity(13);
         for (int K = 1; K <= nplanes; ++K) {
@@ -338,6 +384,7 @@ k_brick2(BrickGrid g, SepTables<T, P + 1> tab, int diag_mode, T* __restrict__ Pv
           B2_TOC(tp, 2);
         }
       }
+#endif
       __syncwarp();
     } else if constexpr (ROLE == 2) {
       // ================================ update warps ================================
