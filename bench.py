@@ -500,8 +500,8 @@ def main():
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
         try:
-            # ncu capture is taken at 73^3 cells (same kernel, same brick shape); DRAM bytes per DoF
-            # are size independent above L2, so the per-launch figure is scaled to this workload
+            # ncu capture of the same kernel at the bench workload (116^3 cells; tools/gpu_traffic116.sh); DRAM bytes
+            # per DoF are size independent above L2, so other sizes scale the per-DoF figure
             tj = json.loads(prof.read_text())
             if args.geometry == "affine" and args.degree == 5 and args.precision == "fp64" and nc == 1:
                 roofline["traffic"] = tj["bytes_per_dof"] * n

@@ -42,12 +42,7 @@ def val(r, k):
     i = h.index(k)
     return float(r[i].replace(',', '')) * {'Gbyte': 1e9, 'Mbyte': 1e6, 'Kbyte': 1e3, 'byte': 1}.get(u[i], 1)
 tr = [val(r, 'dram__bytes_read.sum') + val(r, 'dram__bytes_write.sum') for r in raw[2:]]
-json.dump({"k_brick_merged_bytes_per_launch": sum(tr) / len(tr), "launches": tr,
-           "workload": "73^3 cells Q5 (49027896 DoFs)", "bytes_per_dof": sum(tr) / len(tr) / 49027896,
-           "kernel": "k_brick2<5,double>",
-           "source": "round 2, ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum, two consecutive launches "
-                     "(one with, one without the x update); model 64 / 48 B per DoF on interior DoFs (the separable 1/diag is computed, not loaded)"},
-          open('profiles/traffic.json', 'w'), indent=1)
+# (profiles/traffic.json is written from the 116^3 capture of tools/gpu_traffic116.sh; this 73^3 figure goes to the summary)
 print("traffic B/DoF", [t / 49027896 for t in tr])
 subprocess.run([sys.executable, "tools/ncu_summary.py", "gpurun_out/prof_brick2.ncu-rep", f"profiles/{tag}_ncu_brick2.txt",
                 "k_brick2<5,double> (round 2); 73^3 cells Q5; ncu --set full --clock-control none --import-source on"],
